@@ -1,0 +1,305 @@
+"""bench.py -- MARS batched descents on B200 (BASELINE.json metric: descents/sec).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2_sk2000]
+    python bench.py --impl reference ...      # the reference CPU implementation, same config
+
+A step is one full batch of the workload's descents (cfg2: 65536 MARS descents on dense
+SK N=2000 Gaussian J) -- plan, relax every run to its quench, round, exact energy/cut,
+best-of-R.  ``value`` times the device work with the plan already resident in HBM
+(CUDA events on the library's stream); ``e2e`` times the public API call
+``run_batch(problem, spec)`` end to end (host plan, pinned H2D of the initial states,
+kernels, D2H of the per-run records, index-order aggregation).  Multi-GPU (torchrun):
+every rank runs its own batch of the same size (weak scaling), distinct run indices.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg2_sk2000")
+    ap.add_argument("--runs", type=int, default=0, help="override runs per GPU (profiling)")
+    ap.add_argument("--kernel", default="auto")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-runs", type=int, default=0, help="CPU baseline sample size")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------ helpers
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d["hbm_gbs"], d["bf16_tflops"], d["bf16_tflops_sustained"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_reference_sample(w, runs: int, workers: int):
+    """The compiled reference (oracle/_ref) on the first `runs` run indices of the workload,
+    through mars::run_batch with `workers` threads.  Returns (descents/s, seconds, stats)."""
+    from oracle.oracle import Oracle, params
+    from paper_1907_05124_b200.workloads import build_oracle_problem
+    try:
+        orc = Oracle("ref")
+        kind = "reference"
+    except FileNotFoundError:
+        orc = Oracle("port")
+        kind = "port"
+    p = build_oracle_problem(orc, w)
+    prm = params(0, w.t_max, 1, 1, 1e-4, uniform=True)
+    t0 = time.perf_counter()
+    b = p.run_batch(prm, runs, w.base_seed, workers=workers, spins=False)
+    dt = time.perf_counter() - t0
+    return runs / dt, dt, b, kind
+
+
+def default_cpu_runs(w, cores):
+    # bounded sample (~10-30 s of host work): one descent per host thread for dense N=2000,
+    # more for the cheaper instances
+    per_core = {"cfg1_sk256_pm1": 64, "cfg2_sk2000": 1, "cfg3a_er800": 8, "cfg3b_er2000": 32,
+                "cfg4_ea2d": 4, "cfg4_ea3d": 1, "cfg5_sk16384": 0}.get(w.name, 1)
+    return max(1, per_core * cores)
+
+
+# ------------------------------------------------------------------------ arms
+
+def run_reference(args, w, rank):
+    """--impl reference: the reference's own CPU implementation, rank 0 only."""
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    runs = args.cpu_runs or default_cpu_runs(w, cores)
+    for _ in range(args.warmup):
+        cpu_reference_sample(w, max(1, runs // 4), cores)
+    vals, secs = [], []
+    kind = "reference"
+    for _ in range(args.steps):
+        v, dt, b, kind = cpu_reference_sample(w, runs, cores)
+        vals.append(v)
+        secs.append(dt)
+    value = statistics.mean(vals)
+    sample = (f"first {runs} run indices of {w.name} (same runs the GPU executes), "
+              f"mars::run_batch with {cores} workers")
+    line = {
+        "impl": "reference", "metric": "descents_per_sec", "value": value, "unit": "descents/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * statistics.mean(secs), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "n": w.n, "runs_per_step": runs, "t_max": w.t_max,
+                   "base_seed": w.base_seed, "note": w.note},
+        "cpu_baseline": {"value": value, "unit": "descents/s", "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "descents/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, w, rank, world, local_rank, dist):
+    import numpy as np
+    import torch
+
+    import paper_1907_05124_b200 as mb
+    from paper_1907_05124_b200.workloads import build_problem
+
+    torch.cuda.set_device(local_rank)
+    runs_per_gpu = args.runs or w.runs
+    total_runs = runs_per_gpu * world
+    problem = build_problem(w, device=local_rank, kernel=args.kernel)
+    spec = mb.BatchSpec(w.params(), total_runs, w.base_seed)
+    first = rank * runs_per_gpu
+    batch = mb.DeviceBatch(problem, spec, first, runs_per_gpu)
+    batch.upload()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        batch.execute()
+    barrier()
+    timings = []
+    with ClockSampler(local_rank) as clocks:
+        t_wall = time.perf_counter()
+        for _ in range(args.steps):
+            timings.append(batch.execute())
+        barrier()
+        t_wall = time.perf_counter() - t_wall
+    dev_ms = sum(t["total_ms"] for t in timings)
+    relax_ms = sum(t["relax_ms"] for t in timings) / len(timings)
+    if dist is not None:
+        t = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+    ms_per_step = dev_ms / args.steps
+    value = total_runs / (ms_per_step / 1000.0)
+    rec, best_idx, best_spins = batch.fetch()
+    ok = rec.status == 0
+    sweeps = int(rec.descent_iters[rec.status != 1].sum())
+    best_local = float(rec.energy[ok].min()) if ok.any() else float("nan")
+
+    # ---- e2e through the public API (host plan + H2D + kernels + D2H + aggregation)
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(1):
+            stats = mb.run_batch(problem, mb.BatchSpec(w.params(), total_runs, w.base_seed))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            stats = mb.run_batch(problem, mb.BatchSpec(w.params(), total_runs, w.base_seed))
+        barrier()
+        e2e_s = (time.perf_counter() - t0) / args.steps
+        if dist is not None:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        n = w.n
+        h2d = runs_per_gpu * (4 * n + 8 + 4 + 1)               # s0 fp32, temp, order, status
+        d2h = runs_per_gpu * (1 + 8 + 8 + 8 + 8) + 8 + n        # records + best index/spins
+        e2e = {"value": total_runs / e2e_s, "unit": "descents/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "best_energy": stats.best_energy,
+               "hit_count": stats.hit_count}
+
+    if rank != 0:
+        return
+    hbm, bf16, bf16_sus, src = peaks()
+    nnz = problem.nonzeros()
+    flops_sr = w.flops_per_sweep_run(nnz)
+    achieved_tf = flops_sr * sweeps / (relax_ms / 1000.0) / 1e12
+    dense = w.kind in ("sk_pm1", "sk_gauss")
+    if dense:
+        roof = {"bound": "tensor", "achieved": achieved_tf, "peak": bf16_sus, "unit": "TFLOP/s",
+                "frac": achieved_tf / bf16_sus, "traffic": None,
+                "kernel": f"relax_{problem.kernel()}",
+                "peak_source": f"{src} bf16 sustained (MEASURED_PEAKS.json)",
+                "algorithmic": "2*N^2 flops per sweep-run x total sweeps per launch"}
+    else:
+        gbs = 8.0 * w.n * sweeps / (relax_ms / 1000.0) / 1e9
+        roof = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                "traffic": None, "kernel": f"relax_{problem.kernel()}",
+                "peak_source": f"{src} HBM copy (MEASURED_PEAKS.json)",
+                "algorithmic": "8*N bytes per sweep-run x total sweeps per launch"}
+    cpu = None
+    if not args.no_cpu and world == 1:
+        cores = os.cpu_count() or 1
+        cruns = args.cpu_runs or default_cpu_runs(w, cores)
+        if cruns > 0:
+            v, dt, b, kind = cpu_reference_sample(w, cruns, cores)
+            cpu = {"value": v, "unit": "descents/s", "cores": cores, "kind": kind,
+                   "sample": f"first {cruns} run indices of {w.name} via mars::run_batch, "
+                             f"{cores} workers, {dt:.1f} s",
+                   "sweep_runs_per_s": float(b.descent_iters.sum() / dt),
+                   "best_energy_sample": float(b.stats["best_energy"])}
+    line = {
+        "metric": "descents_per_sec", "value": value, "unit": "descents/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 state/fields, f64 energies", "data": "synthetic",
+        "config": {"workload": w.name, "n": w.n, "runs_per_gpu": runs_per_gpu,
+                   "total_runs": total_runs, "t_range": [0.0, w.t_max], "c_step": 1.0,
+                   "d_min": 1e-4, "base_seed": w.base_seed, "kernel": problem.kernel(),
+                   "grid": timings[0]["grid"], "slots": timings[0]["slots"],
+                   "l2": "inputs larger than L2 (initial states %.0f MB)" % (runs_per_gpu * w.n * 4 / 1e6),
+                   "parallelism": f"runs sharded over {world} GPU(s)", "note": w.note},
+        "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+        "clocks": clocks.summary(), "gpu_launches": int(sum(t["launches"] for t in timings)),
+        "sweep_runs_per_s": sweeps * world / (ms_per_step / 1000.0),
+        "mean_sweeps_per_descent": sweeps / max(1, int((rec.status != 1).sum())),
+        "best_energy": best_local, "relax_ms": relax_ms, "wall_s_timed": t_wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    from paper_1907_05124_b200.workloads import WORKLOADS
+    w = WORKLOADS[args.workload]
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, w, rank)     # rank 0 only; other ranks exit without work
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl")
+        dist = tdist
+    run_b200(args, w, rank, world, local_rank, dist)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,179 @@
+/*
+ * mars_b200.h -- C-ABI of the B200-native MARS batched-descent engine.
+ *
+ * This is the drop-in seam for the reference's batch API.  The reference (a C++20 header
+ * library under /root/reference/proj) has no FFI of its own; the natural replacement point
+ * is `mars::run_batch(const IsingProblem&, const BatchSpec&) -> BatchStats`
+ * (include/mars/runner.hpp:55-56).  Each entry point below names the reference interface
+ * it replaces.  Plain pointers and sizes only; all host arrays are caller-owned.
+ *
+ * Every compute call runs hand-written sm_100a kernels on the problem's device.  There is
+ * no CPU fallback: with no usable CUDA device, problem creation fails with MARS_ERR_CUDA.
+ */
+#ifndef MARS_B200_H
+#define MARS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (C++ wrappers rethrow the reference's exception classes) ---------- */
+enum {
+    MARS_OK = 0,
+    MARS_ERR_INPUT = 1,      /* mars::InputError (errors.hpp:16)                            */
+    MARS_ERR_RUNTIME = 2,    /* mars::Error (errors.hpp:11)                                  */
+    MARS_ERR_CUDA = 3,       /* CUDA runtime failure or no device                            */
+    MARS_ERR_NCCL = 4,       /* reserved for the multi-GPU exchange                          */
+    MARS_ERR_ALL_FAILED = 5  /* "batch failed: no run completed" (runner.cpp:153-155)        */
+};
+
+/* RunStatus (solvers.hpp:95) */
+enum { MARS_RUN_OK = 0, MARS_RUN_SKIPPED = 1, MARS_RUN_DIVERGED = 2 };
+
+/* StartMode (solvers.hpp:18) */
+enum { MARS_GRID_SWEEP = 0, MARS_UNIFORM_RANDOM = 1 };
+
+/* Kernel family selection for a problem handle. AUTO picks by storage (dense vs CSR). */
+enum { MARS_KERNEL_AUTO = 0, MARS_KERNEL_DENSE_SIMT = 1, MARS_KERNEL_CSR = 2,
+       MARS_KERNEL_DENSE_UMMA = 3 };
+
+/* MarsParams (solvers.hpp:20-27).  sweep_cap = 0 means kMarsSweepCap = 10^6
+ * (solvers.hpp:116); a positive value overrides it (fault injection in tests). */
+typedef struct {
+    double t_min, t_max, t_step, c_step, d_min;
+    int32_t start_mode;
+    int32_t reserved;
+    int64_t sweep_cap;
+} mars_params_t;
+
+/* IsingProblem metadata (model.hpp:52-70). */
+typedef struct {
+    int32_t n;
+    int32_t uses_adjacency;  /* CSR storage (edge density < 5%, model.cpp:91)            */
+    int32_t integral;
+    int32_t has_field;
+    double coupling_sum;     /* ordered sum in storage order (model.cpp:20-45)           */
+    int64_t nonzeros;
+    int32_t device;
+    int32_t kernel;          /* MARS_KERNEL_* actually used by mars_run_* on this handle  */
+} mars_problem_info_t;
+
+/* RunResult fields (solvers.hpp:97-106), one entry per run index, caller-allocated.
+ * Any pointer may be NULL.  spins is [count * n] int8 (+1/-1), row per run. */
+typedef struct {
+    uint8_t* status;
+    double* energy;
+    double* cut;
+    double* start_temp;
+    int64_t* descent_iters;
+    double* elapsed_seconds;
+    int8_t* spins;
+} mars_records_t;
+
+/* BatchStats scalars (runner.hpp:29-44); best_index is the run index of best_result. */
+typedef struct {
+    double best_energy, mean_energy, best_cut, mean_cut;
+    int64_t hit_count;
+    double success_probability, total_seconds, mean_seconds_per_run;
+    int64_t best_index, completed_runs, skipped_runs, failed_runs;
+} mars_stats_t;
+
+/* Device-side timing of the last executed batch (CUDA events on the handle's stream). */
+typedef struct {
+    double relax_ms;         /* the persistent relaxation kernel (dominant kernel)          */
+    double energy_ms;        /* round + exact energy/cut kernel                              */
+    double reduce_ms;        /* best-of-R reduction                                          */
+    double total_ms;         /* first to last event of mars_batch_execute                   */
+    int64_t launches;        /* kernels launched by mars_batch_execute                      */
+    int64_t total_sweeps;    /* sum of descent_iters over the batch                          */
+    int32_t grid;            /* CTAs of the relaxation kernel                                */
+    int32_t slots;           /* concurrent descents (run slots) on the device                */
+} mars_timing_t;
+
+typedef struct mars_problem mars_problem_t;
+typedef struct mars_batch mars_batch_t;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* mars_last_error(void);
+
+/* Library / device facts. */
+int mars_device_count(int* out);
+
+/* ---- problem store (IsingProblem, model.hpp:23-101) -------------------------------- */
+
+/* IsingProblem::dense (model.hpp:41, model.cpp:47-72): J is n*n row-major fp64, symmetric
+ * with zero diagonal; h may be NULL.  Copies the couplings to `device` in the layouts the
+ * kernels use.  kernel = MARS_KERNEL_*. */
+int mars_problem_dense(int32_t n, const double* J, const double* h, int32_t device,
+                       int32_t kernel, mars_problem_t** out);
+
+/* IsingProblem::from_edges (model.hpp:46, model.cpp:74-131): same 5% dense/CSR rule. */
+int mars_problem_from_edges(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                            const double* w, const double* h, int32_t device, int32_t kernel,
+                            mars_problem_t** out);
+
+void mars_problem_destroy(mars_problem_t* p);
+int mars_problem_info(const mars_problem_t* p, mars_problem_info_t* out);
+
+/* energy / cut_value of one spin vector, on the device, exact reference order
+ * (model.cpp:203-229). */
+int mars_energy(const mars_problem_t* p, const int8_t* spins, double* energy, double* cut);
+
+/* ---- parameters and plan (solvers.hpp:18-35,133-139; solvers.cpp:35-52,202-227) -------- */
+
+int mars_validate_params(const mars_params_t* prm);                 /* validate(MarsParams) */
+int mars_run_count(const mars_params_t* prm, int64_t requested, int64_t* out);
+int mars_run_plan(const mars_params_t* prm, uint64_t base_seed, int64_t index,
+                  int32_t* skipped, double* start_temp, uint64_t* seed);
+/* The descent's initial state s_i = Rng(seed).uniform_open_sym() (solvers.cpp:184-187). */
+int mars_initial_state(uint64_t seed, int32_t n, double* s);
+uint64_t mars_splitmix64(uint64_t x);                               /* rng.hpp:13  */
+uint64_t mars_sub_seed(uint64_t base_seed, uint64_t run_index);     /* rng.hpp:20  */
+
+/* ---- the batch (run_batch, runner.hpp:55-56 / runner.cpp:170-178) ------------------------
+ *
+ * One call = validate, plan on host threads, H2D of initial states and start
+ * temperatures, persistent relaxation kernel, exact energy/cut kernel, best-of-R
+ * reduction, D2H of the per-run records, and the reference's index-order aggregation
+ * (runner.cpp:126-167).  `runs` has the reference meaning (ignored by GridSweep).
+ * `records` and `best_spins` (n bytes) may be NULL. */
+int mars_run_batch(mars_problem_t* p, const mars_params_t* prm, int64_t runs,
+                   uint64_t base_seed, mars_records_t* records, mars_stats_t* stats,
+                   int8_t* best_spins);
+
+/* A contiguous shard [first, first+count) of the batch's run indices (for multi-GPU:
+ * each rank runs its shard, the records are gathered, then mars_aggregate). */
+int mars_run_shard(mars_problem_t* p, const mars_params_t* prm, int64_t runs,
+                   uint64_t base_seed, int64_t first, int64_t count, mars_records_t* records);
+
+/* The reference's aggregation (runner.cpp:126-167) over `count` records in index order.
+ * energy_tolerance: 0 for integral problems, 1e-9 otherwise (model.hpp:82). */
+int mars_aggregate(int64_t count, const uint8_t* status, const double* energy,
+                   const double* cut, const double* elapsed_seconds, double energy_tolerance,
+                   double total_seconds, mars_stats_t* stats);
+
+/* ---- staged batch (for device-resident timing; mars_run_* are built from these) -------- */
+
+int mars_batch_create(mars_problem_t* p, const mars_params_t* prm, int64_t runs,
+                      uint64_t base_seed, int64_t first, int64_t count, mars_batch_t** out);
+/* Host plan + H2D of the initial states (pinned staging). */
+int mars_batch_upload(mars_batch_t* b);
+/* Device work only (relax -> energy -> reduce), blocks until done; fills timing. */
+int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing);
+/* D2H of the records (and optional per-run spins), best index and best spins. */
+int mars_batch_fetch(mars_batch_t* b, mars_records_t* records, int64_t* best_index,
+                     int8_t* best_spins);
+void mars_batch_destroy(mars_batch_t* b);
+
+/* ---- instance generators built from the reference Rng --------------- */
+void mars_gen_sk_gaussian(int32_t n, uint64_t seed, double* J);     /* io.cpp:151-163 */
+void mars_gen_sk_pm1(int32_t n, uint64_t seed, double* J);
+int64_t mars_gen_er(int32_t n, double prob, uint64_t seed, int32_t* u, int32_t* v, double* w);
+int64_t mars_gen_ea(int32_t L, int32_t dims, uint64_t seed, int32_t* u, int32_t* v, double* w);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,81 @@
+// kernels.cuh -- device-side interface shared by the host driver and the sm_100a kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace marsb200 {
+
+// Run-slot state machine constants (solvers.cpp:19, solvers.hpp:116).
+constexpr double kTempFloor = 1e-12;
+constexpr std::int64_t kSweepCap = 1000000;
+
+// Everything the persistent relaxation kernels need.  One launch relaxes `queue_len`
+// descents: slots pull queue positions from an atomic counter, so the longest-expected
+// runs (highest start temperature, placed first by the host) start first.
+struct RelaxArgs {
+    int n;             // spins
+    int np;            // padded spins (multiple of the kernel's block size)
+    // dense couplings, fp32 row-major [np][np], zero padded
+    const float* J32;
+    // CSR couplings (neighbours sorted ascending, model.cpp:116-127)
+    const int* off;
+    const int* idx;
+    const float* w32;
+    const float* h32;          // [n] external field, or nullptr
+    // the runs of this launch
+    int queue_len;             // descents to run
+    const int* order;          // [queue_len] local run index, processing order
+    const float* s0;           // [count][n] initial states (fp32 of the fp64 draws)
+    const double* start_temp;  // [count]
+    double c_step, d_min;
+    long long sweep_cap;
+    // scratch
+    float* work;               // per-CTA slot state, kernel-specific layout
+    int* queue_head;           // atomic counter, zero before launch
+    // per-run outputs (local run index)
+    std::uint8_t* status;
+    long long* iters;
+    double* elapsed;
+    std::int8_t* spins;        // [count][n] rounded final state (round_spins, model.cpp:245)
+};
+
+// Exact-order energy evaluation (model.cpp:203-229) over `count` rounded spin vectors.
+struct EnergyArgs {
+    int n;
+    const double* J64;         // dense [n][n] fp64 (reference order), or nullptr
+    const int* off;
+    const int* idx;
+    const double* w64;         // CSR weights fp64
+    const double* h64;         // [n] or nullptr
+    double coupling_sum;
+    long long count;
+    const std::int8_t* spins;  // [count][n]
+    const std::uint8_t* status;
+    double* energy;
+    double* cut;
+};
+
+struct BestArgs {
+    long long count;
+    const std::uint8_t* status;
+    const double* energy;
+    double* part_energy;       // [grid]
+    long long* part_index;     // [grid]
+    long long* best_index;     // [1]
+};
+
+// Launchers (return cudaGetLastError()).
+cudaError_t launch_relax_dense_simt(const RelaxArgs& a, int grid, cudaStream_t st);
+int relax_dense_simt_slots_per_cta();
+int relax_dense_simt_block();
+std::size_t relax_dense_simt_work_floats(int np);
+
+cudaError_t launch_relax_csr(const RelaxArgs& a, int grid, cudaStream_t st);
+int relax_csr_slots_per_cta();
+std::size_t relax_csr_work_floats(int np);
+
+cudaError_t launch_energy(const EnergyArgs& a, cudaStream_t st);
+cudaError_t launch_best(const BestArgs& a, int grid, cudaStream_t st);
+
+}  // namespace marsb200

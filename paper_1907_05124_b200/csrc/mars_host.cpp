@@ -1,0 +1,905 @@
+// mars_host.cpp -- C-ABI implementation (include/mars_b200.h): the coupling store, the
+// host-side plan, the staged batch driver and the reference's index-order aggregation.
+//
+// Host responsibilities mirror the reference's non-kernel code:
+//   validate / run_count / run_plan     solvers.cpp:35-52, 202-227
+//   IsingProblem construction+metadata  model.cpp:20-131
+//   run_batch / run_batch_with          runner.cpp:81-178 (aggregation 126-167)
+// The per-run work itself (descents, energies, best-of-R) runs in the sm_100a kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <utility>
+#include <vector>
+
+#include "../../include/mars_b200.h"
+#include "kernels.cuh"
+#include "rng.hpp"
+
+using namespace marsb200;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+    do {                                                                                   \
+        const cudaError_t e_ = (expr);                                                     \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(MARS_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+constexpr double kSparseDensityThreshold = 0.05;      // model.hpp:31
+constexpr std::uint64_t kStartTempTag = 0x74656d7073746172ull;  // solvers.cpp:23
+
+bool is_integral_value(double v) { return std::nearbyint(v) == v && std::isfinite(v); }
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+int host_threads() {
+    const unsigned hc = std::thread::hardware_concurrency();
+    return static_cast<int>(std::max(1u, std::min(hc, 64u)));
+}
+
+template <class F>
+void parallel_for(std::int64_t count, F&& f) {
+    const int nt = static_cast<int>(std::min<std::int64_t>(host_threads(), std::max<std::int64_t>(count / 64, 1)));
+    if (nt <= 1) {
+        f(0, count);
+        return;
+    }
+    std::vector<std::thread> th;
+    const std::int64_t chunk = (count + nt - 1) / nt;
+    for (int t = 0; t < nt; ++t) {
+        const std::int64_t lo = t * chunk, hi = std::min(count, lo + chunk);
+        if (lo < hi) th.emplace_back([&f, lo, hi] { f(lo, hi); });
+    }
+    for (auto& x : th) x.join();
+}
+
+// solvers.cpp:35-41
+int check_params(const mars_params_t* p) {
+    if (!p) return fail(MARS_ERR_INPUT, "mars: null parameters");
+    if (!(p->t_min >= 0.0)) return fail(MARS_ERR_INPUT, "mars: t_min must be >= 0");
+    if (!(p->t_max > p->t_min)) return fail(MARS_ERR_INPUT, "mars: t_max must exceed t_min");
+    if (!(p->t_step > 0.0)) return fail(MARS_ERR_INPUT, "mars: t_step must be positive");
+    if (!(p->c_step > 0.0)) return fail(MARS_ERR_INPUT, "mars: c_step must be positive");
+    if (!(p->d_min > 0.0)) return fail(MARS_ERR_INPUT, "mars: d_min must be positive");
+    if (p->start_mode != MARS_GRID_SWEEP && p->start_mode != MARS_UNIFORM_RANDOM)
+        return fail(MARS_ERR_INPUT, "mars: unknown start mode");
+    if (p->sweep_cap < 0) return fail(MARS_ERR_INPUT, "mars: sweep_cap must be >= 0");
+    return MARS_OK;
+}
+
+// solvers.cpp:215-227 (GridSweep slot k at t_min + k*t_step; UniformRandom via the tagged stream)
+void plan_of(const mars_params_t* prm, std::uint64_t base, std::int64_t idx, bool* skipped,
+             double* t, std::uint64_t* seed) {
+    *seed = sub_seed(base, static_cast<std::uint64_t>(idx));
+    if (prm->start_mode == MARS_GRID_SWEEP) {
+        *t = prm->t_min + static_cast<double>(idx) * prm->t_step;
+        *skipped = !(*t > 0.0);
+    } else {
+        Stream r(splitmix64(*seed ^ kStartTempTag));
+        *t = prm->t_min + r.open01() * (prm->t_max - prm->t_min);
+        *skipped = false;
+    }
+}
+
+}  // namespace
+
+// ============================================================================ problem store
+
+struct mars_problem {
+    int n = 0;
+    bool dense = true;              // storage choice of the reference (model.cpp:91)
+    bool integral = true;
+    bool has_field = false;
+    double coupling_sum = 0.0;
+    std::int64_t nnz = 0;
+    int device = 0;
+    int kernel = MARS_KERNEL_DENSE_SIMT;
+    int np = 0;                     // padded size for the dense kernels
+    int num_sms = 148;
+    std::vector<double> J;          // dense row-major (dense storage)
+    std::vector<int> off, idx;      // CSR (adjacency storage)
+    std::vector<double> wt;
+    std::vector<double> h;
+    cudaStream_t stream = nullptr;
+    // device copies
+    float* dJ32 = nullptr;          // [np][np] fp32, zero padded (dense kernels)
+    double* dJ64 = nullptr;         // [n][n]   fp64 (exact energy, dense storage)
+    int* dOff = nullptr;
+    int* dIdx = nullptr;
+    float* dW32 = nullptr;
+    double* dW64 = nullptr;
+    float* dH32 = nullptr;
+    double* dH64 = nullptr;
+
+    ~mars_problem() {
+        cudaSetDevice(device);
+        cudaFree(dJ32);
+        cudaFree(dJ64);
+        cudaFree(dOff);
+        cudaFree(dIdx);
+        cudaFree(dW32);
+        cudaFree(dW64);
+        cudaFree(dH32);
+        cudaFree(dH64);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+// model.cpp:20-45 -- metadata in storage order
+void finalize_metadata(mars_problem* p) {
+    p->coupling_sum = 0.0;
+    p->nnz = 0;
+    p->integral = true;
+    if (p->dense) {
+        for (std::size_t k = 0; k < p->J.size(); ++k) {
+            const double w = p->J[k];
+            p->coupling_sum += w;
+            if (w != 0.0) ++p->nnz;
+            if (p->integral && !is_integral_value(w)) p->integral = false;
+        }
+    } else {
+        for (double w : p->wt) {
+            p->coupling_sum += w;
+            ++p->nnz;
+            if (p->integral && !is_integral_value(w)) p->integral = false;
+        }
+    }
+    p->has_field = false;
+    for (double v : p->h) {
+        if (v != 0.0) p->has_field = true;
+        if (p->integral && !is_integral_value(v)) p->integral = false;
+    }
+}
+
+template <class T>
+int upload(T** dst, const T* src, std::size_t count) {
+    CUDA_TRY(cudaMalloc(dst, std::max<std::size_t>(count, 1) * sizeof(T)));
+    if (count) CUDA_TRY(cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    return MARS_OK;
+}
+
+int resolve_kernel(mars_problem* p, int requested) {
+    if (requested == MARS_KERNEL_AUTO) return p->dense ? MARS_KERNEL_DENSE_SIMT : MARS_KERNEL_CSR;
+    if (requested == MARS_KERNEL_DENSE_SIMT || requested == MARS_KERNEL_CSR) return requested;
+    return -1;
+}
+
+// Device copies in the layouts the kernels use.
+int build_device_store(mars_problem* p) {
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (p->device < 0 || p->device >= ndev)
+        return fail(MARS_ERR_CUDA, "device " + std::to_string(p->device) + " not present (" +
+                                       std::to_string(ndev) + " visible)");
+    CUDA_TRY(cudaSetDevice(p->device));
+    CUDA_TRY(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device));
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    const int n = p->n;
+    // exact-order energy operands (reference storage)
+    if (p->dense) {
+        if (int rc = upload(&p->dJ64, p->J.data(), p->J.size())) return rc;
+    } else {
+        if (int rc = upload(&p->dOff, p->off.data(), p->off.size())) return rc;
+        if (int rc = upload(&p->dIdx, p->idx.data(), p->idx.size())) return rc;
+        if (int rc = upload(&p->dW64, p->wt.data(), p->wt.size())) return rc;
+    }
+    if (p->has_field) {
+        std::vector<float> h32(p->h.begin(), p->h.end());
+        if (int rc = upload(&p->dH64, p->h.data(), p->h.size())) return rc;
+        if (int rc = upload(&p->dH32, h32.data(), h32.size())) return rc;
+    }
+    // relaxation operands
+    if (p->kernel == MARS_KERNEL_DENSE_SIMT) {
+        p->np = round_up(n, relax_dense_simt_block());
+        std::vector<float> j32(static_cast<std::size_t>(p->np) * p->np, 0.0f);
+        if (p->dense) {
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < n; ++j)
+                    j32[static_cast<std::size_t>(i) * p->np + j] =
+                        static_cast<float>(p->J[static_cast<std::size_t>(i) * n + j]);
+        } else {
+            for (int i = 0; i < n; ++i)
+                for (int k = p->off[i]; k < p->off[i + 1]; ++k)
+                    j32[static_cast<std::size_t>(i) * p->np + p->idx[k]] += static_cast<float>(p->wt[k]);
+        }
+        if (int rc = upload(&p->dJ32, j32.data(), j32.size())) return rc;
+    } else {
+        p->np = n;
+        std::vector<int> off, idx;
+        std::vector<float> w32;
+        if (p->dense) {  // CSR view of a dense store, ascending columns (row_dot order minus zeros)
+            off.assign(n + 1, 0);
+            for (int i = 0; i < n; ++i) {
+                for (int j = 0; j < n; ++j) {
+                    const double w = p->J[static_cast<std::size_t>(i) * n + j];
+                    if (w != 0.0) {
+                        idx.push_back(j);
+                        w32.push_back(static_cast<float>(w));
+                    }
+                }
+                off[i + 1] = static_cast<int>(idx.size());
+            }
+            if (int rc = upload(&p->dOff, off.data(), off.size())) return rc;
+            if (int rc = upload(&p->dIdx, idx.data(), idx.size())) return rc;
+        } else {
+            w32.assign(p->wt.begin(), p->wt.end());
+        }
+        if (int rc = upload(&p->dW32, w32.data(), w32.size())) return rc;
+    }
+    return MARS_OK;
+}
+
+int finish_problem(mars_problem* p, int device, int kernel, mars_problem_t** out) {
+    p->device = device;
+    p->kernel = resolve_kernel(p, kernel);
+    if (p->kernel < 0) {
+        delete p;
+        return fail(MARS_ERR_INPUT, "unknown kernel selection " + std::to_string(kernel));
+    }
+    finalize_metadata(p);
+    if (int rc = build_device_store(p)) {
+        delete p;
+        return rc;
+    }
+    *out = p;
+    return MARS_OK;
+}
+
+}  // namespace
+
+// ============================================================================ batch
+
+struct mars_batch {
+    mars_problem* p = nullptr;
+    mars_params_t prm{};
+    std::int64_t runs = 0;          // effective batch size (run_count)
+    std::uint64_t base_seed = 0;
+    std::int64_t first = 0, count = 0;
+    int queue_len = 0;
+    int grid = 0, slots = 0;
+    bool uploaded = false, executed = false;
+    // host plan
+    std::vector<std::uint8_t> skipped;
+    std::vector<double> temp;
+    float* h_s0 = nullptr;          // pinned [count][n]
+    int* h_order = nullptr;         // pinned [count]
+    double* h_temp = nullptr;       // pinned [count]
+    std::uint8_t* h_status = nullptr;  // pinned [count]
+    // device
+    float* d_s0 = nullptr;
+    double* d_temp = nullptr;
+    int* d_order = nullptr;
+    float* d_work = nullptr;
+    std::size_t work_floats = 0;
+    int* d_queue = nullptr;
+    std::uint8_t* d_status = nullptr;
+    long long* d_iters = nullptr;
+    double* d_elapsed = nullptr;
+    std::int8_t* d_spins = nullptr;
+    double* d_energy = nullptr;
+    double* d_cut = nullptr;
+    double* d_part_e = nullptr;
+    long long* d_part_i = nullptr;
+    long long* d_best = nullptr;
+    int best_grid = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+    ~mars_batch() {
+        if (!p) return;
+        cudaSetDevice(p->device);
+        cudaFreeHost(h_s0);
+        cudaFreeHost(h_order);
+        cudaFreeHost(h_temp);
+        cudaFreeHost(h_status);
+        cudaFree(d_s0);
+        cudaFree(d_temp);
+        cudaFree(d_order);
+        cudaFree(d_work);
+        cudaFree(d_queue);
+        cudaFree(d_status);
+        cudaFree(d_iters);
+        cudaFree(d_elapsed);
+        cudaFree(d_spins);
+        cudaFree(d_energy);
+        cudaFree(d_cut);
+        cudaFree(d_part_e);
+        cudaFree(d_part_i);
+        cudaFree(d_best);
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+namespace {
+
+int batch_alloc(mars_batch* b) {
+    mars_problem* p = b->p;
+    const std::size_t cnt = static_cast<std::size_t>(std::max<std::int64_t>(b->count, 1));
+    const std::size_t n = static_cast<std::size_t>(p->n);
+    CUDA_TRY(cudaSetDevice(p->device));
+    CUDA_TRY(cudaMallocHost(&b->h_s0, cnt * n * sizeof(float)));
+    CUDA_TRY(cudaMallocHost(&b->h_order, cnt * sizeof(int)));
+    CUDA_TRY(cudaMallocHost(&b->h_temp, cnt * sizeof(double)));
+    CUDA_TRY(cudaMallocHost(&b->h_status, cnt));
+    CUDA_TRY(cudaMalloc(&b->d_s0, cnt * n * sizeof(float)));
+    CUDA_TRY(cudaMalloc(&b->d_temp, cnt * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&b->d_order, cnt * sizeof(int)));
+    CUDA_TRY(cudaMalloc(&b->d_queue, sizeof(int)));
+    CUDA_TRY(cudaMalloc(&b->d_status, cnt));
+    CUDA_TRY(cudaMalloc(&b->d_iters, cnt * sizeof(long long)));
+    CUDA_TRY(cudaMalloc(&b->d_elapsed, cnt * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&b->d_spins, cnt * n));
+    CUDA_TRY(cudaMalloc(&b->d_energy, cnt * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&b->d_cut, cnt * sizeof(double)));
+    b->best_grid = static_cast<int>(std::min<std::int64_t>((b->count + 255) / 256, 2 * p->num_sms));
+    b->best_grid = std::max(b->best_grid, 1);
+    CUDA_TRY(cudaMalloc(&b->d_part_e, b->best_grid * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&b->d_part_i, b->best_grid * sizeof(long long)));
+    CUDA_TRY(cudaMalloc(&b->d_best, sizeof(long long)));
+    for (auto& e : b->ev) CUDA_TRY(cudaEventCreate(&e));
+    // plan (host, cheap) decides the queue length and hence the grid
+    b->skipped.assign(cnt, 0);
+    b->temp.assign(cnt, 0.0);
+    std::vector<std::uint64_t> seeds(cnt);
+    parallel_for(b->count, [&](std::int64_t lo, std::int64_t hi) {
+        for (std::int64_t k = lo; k < hi; ++k) {
+            bool sk;
+            plan_of(&b->prm, b->base_seed, b->first + k, &sk, &b->temp[k], &seeds[k]);
+            b->skipped[k] = sk;
+        }
+    });
+    std::vector<int> order;
+    for (std::int64_t k = 0; k < b->count; ++k)
+        if (!b->skipped[k]) order.push_back(static_cast<int>(k));
+    // longest-expected descents first: the level count grows with the start temperature
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int x, int y) { return b->temp[x] > b->temp[y]; });
+    b->queue_len = static_cast<int>(order.size());
+    std::copy(order.begin(), order.end(), b->h_order);
+    for (std::int64_t k = 0; k < b->count; ++k) {
+        b->h_temp[k] = b->temp[k];
+        b->h_status[k] = b->skipped[k] ? MARS_RUN_SKIPPED : 255;
+    }
+    int tm = 1;
+    std::size_t per_cta = 0;
+    int max_grid = p->num_sms;
+    if (p->kernel == MARS_KERNEL_DENSE_SIMT) {
+        tm = relax_dense_simt_slots_per_cta();
+        per_cta = relax_dense_simt_work_floats(p->np);
+    } else {
+        tm = relax_csr_slots_per_cta();
+        per_cta = relax_csr_work_floats(p->np);
+        max_grid = 8 * p->num_sms;
+    }
+    b->grid = std::max(1, std::min(max_grid, (b->queue_len + tm - 1) / tm));
+    b->slots = b->grid * tm;
+    b->work_floats = per_cta * b->grid;
+    CUDA_TRY(cudaMalloc(&b->d_work, b->work_floats * sizeof(float)));
+    return MARS_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C-ABI
+
+extern "C" {
+
+const char* mars_last_error(void) { return g_err.c_str(); }
+
+int mars_device_count(int* out) {
+    CUDA_TRY(cudaGetDeviceCount(out));
+    return MARS_OK;
+}
+
+uint64_t mars_splitmix64(uint64_t x) { return splitmix64(x); }
+uint64_t mars_sub_seed(uint64_t b, uint64_t i) { return sub_seed(b, i); }
+
+int mars_validate_params(const mars_params_t* prm) { return check_params(prm); }
+
+// solvers.cpp:202-213 (+ mars_grid_count 43-48)
+int mars_run_count(const mars_params_t* prm, int64_t requested, int64_t* out) {
+    if (int rc = check_params(prm)) return rc;
+    if (prm->start_mode == MARS_GRID_SWEEP) {
+        const double slots = std::floor((prm->t_max - prm->t_min) / prm->t_step);
+        if (!(slots >= 0.0) || slots > 1e9)
+            return fail(MARS_ERR_INPUT, "mars: grid of " + std::to_string(slots) +
+                                            " temperatures is not usable");
+        const std::int64_t count = static_cast<std::int64_t>(slots) + 1;
+        if (count == 1 && !(prm->t_min > 0.0))
+            return fail(MARS_ERR_INPUT,
+                        "mars: the temperature grid contains no positive starting temperature");
+        *out = count;
+        return MARS_OK;
+    }
+    if (requested < 1) return fail(MARS_ERR_INPUT, "mars: UniformRandom mode needs runs >= 1");
+    *out = requested;
+    return MARS_OK;
+}
+
+int mars_run_plan(const mars_params_t* prm, uint64_t base_seed, int64_t index, int32_t* skipped,
+                  double* start_temp, uint64_t* seed) {
+    if (int rc = check_params(prm)) return rc;
+    bool sk;
+    plan_of(prm, base_seed, index, &sk, start_temp, seed);
+    *skipped = sk;
+    return MARS_OK;
+}
+
+int mars_initial_state(uint64_t seed, int32_t n, double* s) {
+    Stream r(seed);
+    for (int i = 0; i < n; ++i) s[i] = r.open_sym();
+    return MARS_OK;
+}
+
+int mars_problem_dense(int32_t n, const double* J, const double* h, int32_t device,
+                       int32_t kernel, mars_problem_t** out) {
+    if (n <= 0) return fail(MARS_ERR_INPUT, "problem size must be positive");
+    if (!J || !out) return fail(MARS_ERR_INPUT, "null argument");
+    for (int i = 0; i < n; ++i) {                                          // model.cpp:55-64
+        if (J[static_cast<std::size_t>(i) * n + i] != 0.0)
+            return fail(MARS_ERR_INPUT, "coupling diagonal must be zero (row " + std::to_string(i) + ")");
+        for (int j = i + 1; j < n; ++j)
+            if (J[static_cast<std::size_t>(i) * n + j] != J[static_cast<std::size_t>(j) * n + i])
+                return fail(MARS_ERR_INPUT, "coupling matrix must be symmetric (entries " +
+                                                std::to_string(i) + "," + std::to_string(j) + ")");
+    }
+    auto* p = new mars_problem;
+    p->n = n;
+    p->dense = true;
+    p->J.assign(J, J + static_cast<std::size_t>(n) * n);
+    p->h.assign(n, 0.0);
+    if (h) std::copy(h, h + n, p->h.begin());
+    return finish_problem(p, device, kernel, out);
+}
+
+int mars_problem_from_edges(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                            const double* w, const double* h, int32_t device, int32_t kernel,
+                            mars_problem_t** out) {
+    if (n <= 0) return fail(MARS_ERR_INPUT, "problem size must be positive");
+    if (!out || (m > 0 && (!u || !v || !w))) return fail(MARS_ERR_INPUT, "null argument");
+    for (std::int64_t k = 0; k < m; ++k) {                                  // model.cpp:80-84
+        if (u[k] < 0 || u[k] >= n || v[k] < 0 || v[k] >= n)
+            return fail(MARS_ERR_INPUT, "edge endpoint out of range");
+        if (u[k] == v[k]) return fail(MARS_ERR_INPUT, "self-coupling is not allowed");
+    }
+    auto* p = new mars_problem;
+    p->n = n;
+    p->h.assign(n, 0.0);
+    if (h) std::copy(h, h + n, p->h.begin());
+    const double max_pairs = 0.5 * static_cast<double>(n) * (n - 1);
+    const double density = max_pairs > 0 ? static_cast<double>(m) / max_pairs : 1.0;
+    if (density >= kSparseDensityThreshold) {                               // model.cpp:91-98
+        p->dense = true;
+        p->J.assign(static_cast<std::size_t>(n) * n, 0.0);
+        for (std::int64_t k = 0; k < m; ++k) {
+            p->J[static_cast<std::size_t>(u[k]) * n + v[k]] += w[k];
+            p->J[static_cast<std::size_t>(v[k]) * n + u[k]] += w[k];
+        }
+    } else {                                                                // model.cpp:99-128
+        p->dense = false;
+        std::vector<int> deg(n, 0);
+        for (std::int64_t k = 0; k < m; ++k) {
+            ++deg[u[k]];
+            ++deg[v[k]];
+        }
+        p->off.assign(n + 1, 0);
+        for (int i = 0; i < n; ++i) p->off[i + 1] = p->off[i] + deg[i];
+        p->idx.resize(2 * m);
+        p->wt.resize(2 * m);
+        std::vector<int> cur(p->off.begin(), p->off.end() - 1);
+        for (std::int64_t k = 0; k < m; ++k) {
+            p->idx[cur[u[k]]] = v[k];
+            p->wt[cur[u[k]]++] = w[k];
+            p->idx[cur[v[k]]] = u[k];
+            p->wt[cur[v[k]]++] = w[k];
+        }
+        std::vector<std::pair<int, double>> row;
+        for (int i = 0; i < n; ++i) {                                       // canonical order
+            row.clear();
+            for (int k = p->off[i]; k < p->off[i + 1]; ++k) row.emplace_back(p->idx[k], p->wt[k]);
+            std::sort(row.begin(), row.end());
+            for (int k = p->off[i]; k < p->off[i + 1]; ++k) {
+                p->idx[k] = row[k - p->off[i]].first;
+                p->wt[k] = row[k - p->off[i]].second;
+            }
+        }
+    }
+    return finish_problem(p, device, kernel, out);
+}
+
+void mars_problem_destroy(mars_problem_t* p) { delete p; }
+
+int mars_problem_info(const mars_problem_t* p, mars_problem_info_t* out) {
+    if (!p || !out) return fail(MARS_ERR_INPUT, "null argument");
+    out->n = p->n;
+    out->uses_adjacency = !p->dense;
+    out->integral = p->integral;
+    out->has_field = p->has_field;
+    out->coupling_sum = p->coupling_sum;
+    out->nonzeros = p->nnz;
+    out->device = p->device;
+    out->kernel = p->kernel;
+    return MARS_OK;
+}
+
+int mars_energy(const mars_problem_t* p, const int8_t* spins, double* energy, double* cut) {
+    if (!p || !spins) return fail(MARS_ERR_INPUT, "null argument");
+    for (int i = 0; i < p->n; ++i)
+        if (spins[i] != 1 && spins[i] != -1) return fail(MARS_ERR_INPUT, "spins must be +1/-1");
+    CUDA_TRY(cudaSetDevice(p->device));
+    std::int8_t* ds = nullptr;
+    std::uint8_t* dst = nullptr;
+    double* dout = nullptr;
+    CUDA_TRY(cudaMalloc(&ds, p->n));
+    CUDA_TRY(cudaMalloc(&dst, 1));
+    CUDA_TRY(cudaMalloc(&dout, 2 * sizeof(double)));
+    CUDA_TRY(cudaMemcpyAsync(ds, spins, p->n, cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(cudaMemsetAsync(dst, 0, 1, p->stream));
+    EnergyArgs ea{p->n, p->dJ64, p->dOff, p->dIdx, p->dW64, p->dH64, p->coupling_sum, 1, ds,
+                  dst, dout, dout + 1};
+    CUDA_TRY(launch_energy(ea, p->stream));
+    double out[2];
+    CUDA_TRY(cudaMemcpyAsync(out, dout, sizeof out, cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    cudaFree(ds);
+    cudaFree(dst);
+    cudaFree(dout);
+    if (energy) *energy = out[0];
+    if (cut) *cut = out[1];
+    return MARS_OK;
+}
+
+int mars_batch_create(mars_problem_t* p, const mars_params_t* prm, int64_t runs,
+                      uint64_t base_seed, int64_t first, int64_t count, mars_batch_t** out) {
+    if (!p || !out) return fail(MARS_ERR_INPUT, "null argument");
+    std::int64_t total = 0;
+    if (int rc = mars_run_count(prm, runs, &total)) return rc;
+    if (first < 0 || count < 0 || first + count > total)
+        return fail(MARS_ERR_INPUT, "shard [" + std::to_string(first) + ", " +
+                                        std::to_string(first + count) + ") outside the batch of " +
+                                        std::to_string(total) + " runs");
+    auto* b = new mars_batch;
+    b->p = p;
+    b->prm = *prm;
+    if (b->prm.sweep_cap == 0) b->prm.sweep_cap = kSweepCap;
+    b->runs = total;
+    b->base_seed = base_seed;
+    b->first = first;
+    b->count = count;
+    if (int rc = batch_alloc(b)) {
+        delete b;
+        return rc;
+    }
+    *out = b;
+    return MARS_OK;
+}
+
+// Initial states: s_i = Rng(seed).uniform_open_sym(), i ascending (solvers.cpp:184-187),
+// generated on host threads straight into pinned memory, then one H2D copy per array.
+int mars_batch_upload(mars_batch_t* b) {
+    if (!b) return fail(MARS_ERR_INPUT, "null argument");
+    mars_problem* p = b->p;
+    const int n = p->n;
+    parallel_for(b->count, [&](std::int64_t lo, std::int64_t hi) {
+        for (std::int64_t k = lo; k < hi; ++k) {
+            if (b->skipped[k]) continue;
+            Stream r(sub_seed(b->base_seed, static_cast<std::uint64_t>(b->first + k)));
+            float* row = b->h_s0 + static_cast<std::size_t>(k) * n;
+            for (int i = 0; i < n; ++i) row[i] = static_cast<float>(r.open_sym());
+        }
+    });
+    CUDA_TRY(cudaSetDevice(p->device));
+    const std::size_t cnt = static_cast<std::size_t>(b->count);
+    CUDA_TRY(cudaMemcpyAsync(b->d_s0, b->h_s0, cnt * n * sizeof(float), cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(b->d_temp, b->h_temp, cnt * sizeof(double), cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(b->d_order, b->h_order, std::max(b->queue_len, 1) * sizeof(int),
+                             cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(b->d_status, b->h_status, cnt, cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    b->uploaded = true;
+    b->executed = false;
+    return MARS_OK;
+}
+
+int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
+    if (!b) return fail(MARS_ERR_INPUT, "null argument");
+    if (!b->uploaded) return fail(MARS_ERR_RUNTIME, "batch executed before upload");
+    mars_problem* p = b->p;
+    cudaStream_t st = p->stream;
+    CUDA_TRY(cudaSetDevice(p->device));
+    if (b->executed)  // re-execution: restore the pending statuses
+        CUDA_TRY(cudaMemcpyAsync(b->d_status, b->h_status, b->count, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(b->d_queue, 0, sizeof(int), st));
+    CUDA_TRY(cudaMemsetAsync(b->d_work, 0, b->work_floats * sizeof(float), st));
+    RelaxArgs ra{};
+    ra.n = p->n;
+    ra.np = p->np;
+    ra.J32 = p->dJ32;
+    ra.off = p->dOff;
+    ra.idx = p->dIdx;
+    ra.w32 = p->dW32;
+    ra.h32 = p->dH32;
+    ra.queue_len = b->queue_len;
+    ra.order = b->d_order;
+    ra.s0 = b->d_s0;
+    ra.start_temp = b->d_temp;
+    ra.c_step = b->prm.c_step;
+    ra.d_min = b->prm.d_min;
+    ra.sweep_cap = b->prm.sweep_cap;
+    ra.work = b->d_work;
+    ra.queue_head = b->d_queue;
+    ra.status = b->d_status;
+    ra.iters = b->d_iters;
+    ra.elapsed = b->d_elapsed;
+    ra.spins = b->d_spins;
+    std::int64_t launches = 0;
+    CUDA_TRY(cudaEventRecord(b->ev[0], st));
+    if (b->queue_len > 0) {
+        if (p->kernel == MARS_KERNEL_DENSE_SIMT)
+            CUDA_TRY(launch_relax_dense_simt(ra, b->grid, st));
+        else
+            CUDA_TRY(launch_relax_csr(ra, b->grid, st));
+        ++launches;
+    }
+    CUDA_TRY(cudaEventRecord(b->ev[1], st));
+    EnergyArgs ea{p->n, p->dJ64, p->dOff, p->dIdx, p->dW64, p->dH64, p->coupling_sum,
+                  b->count, b->d_spins, b->d_status, b->d_energy, b->d_cut};
+    if (b->count > 0) {
+        CUDA_TRY(launch_energy(ea, st));
+        ++launches;
+    }
+    CUDA_TRY(cudaEventRecord(b->ev[2], st));
+    BestArgs ba{b->count, b->d_status, b->d_energy, b->d_part_e, b->d_part_i, b->d_best};
+    CUDA_TRY(launch_best(ba, b->best_grid, st));
+    launches += 2;
+    CUDA_TRY(cudaEventRecord(b->ev[3], st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    b->executed = true;
+    if (timing) {
+        float ms[3];
+        CUDA_TRY(cudaEventElapsedTime(&ms[0], b->ev[0], b->ev[1]));
+        CUDA_TRY(cudaEventElapsedTime(&ms[1], b->ev[1], b->ev[2]));
+        CUDA_TRY(cudaEventElapsedTime(&ms[2], b->ev[2], b->ev[3]));
+        timing->relax_ms = ms[0];
+        timing->energy_ms = ms[1];
+        timing->reduce_ms = ms[2];
+        timing->total_ms = static_cast<double>(ms[0]) + ms[1] + ms[2];
+        timing->launches = launches;
+        timing->grid = b->grid;
+        timing->slots = b->slots;
+        std::vector<long long> it(static_cast<std::size_t>(b->count));
+        std::vector<std::uint8_t> stt(static_cast<std::size_t>(b->count));
+        if (b->count) {
+            CUDA_TRY(cudaMemcpy(it.data(), b->d_iters, b->count * sizeof(long long), cudaMemcpyDeviceToHost));
+            CUDA_TRY(cudaMemcpy(stt.data(), b->d_status, b->count, cudaMemcpyDeviceToHost));
+        }
+        long long tot = 0;
+        for (std::int64_t k = 0; k < b->count; ++k)
+            if (stt[k] != MARS_RUN_SKIPPED) tot += it[k];
+        timing->total_sweeps = tot;
+    }
+    return MARS_OK;
+}
+
+int mars_batch_fetch(mars_batch_t* b, mars_records_t* rec, int64_t* best_index,
+                     int8_t* best_spins) {
+    if (!b) return fail(MARS_ERR_INPUT, "null argument");
+    if (!b->executed) return fail(MARS_ERR_RUNTIME, "batch fetched before execute");
+    mars_problem* p = b->p;
+    cudaStream_t st = p->stream;
+    const std::size_t cnt = static_cast<std::size_t>(b->count);
+    CUDA_TRY(cudaSetDevice(p->device));
+    std::vector<std::uint8_t> status(cnt);
+    std::vector<long long> iters(cnt);
+    if (cnt) {
+        CUDA_TRY(cudaMemcpyAsync(status.data(), b->d_status, cnt, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(iters.data(), b->d_iters, cnt * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    }
+    if (rec) {
+        if (rec->energy && cnt) CUDA_TRY(cudaMemcpyAsync(rec->energy, b->d_energy, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (rec->cut && cnt) CUDA_TRY(cudaMemcpyAsync(rec->cut, b->d_cut, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (rec->elapsed_seconds && cnt) CUDA_TRY(cudaMemcpyAsync(rec->elapsed_seconds, b->d_elapsed, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (rec->spins && cnt) CUDA_TRY(cudaMemcpyAsync(rec->spins, b->d_spins, cnt * p->n, cudaMemcpyDeviceToHost, st));
+    }
+    long long best = -1;
+    CUDA_TRY(cudaMemcpyAsync(&best, b->d_best, sizeof best, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (best >= 0 && best_spins)
+        CUDA_TRY(cudaMemcpy(best_spins, b->d_spins + static_cast<std::size_t>(best) * p->n, p->n, cudaMemcpyDeviceToHost));
+    for (std::size_t k = 0; k < cnt; ++k)
+        if (status[k] > MARS_RUN_DIVERGED)
+            return fail(MARS_ERR_RUNTIME, "run " + std::to_string(b->first + k) + " was never executed");
+    if (rec) {
+        if (rec->status) std::copy(status.begin(), status.end(), rec->status);
+        if (rec->descent_iters)
+            for (std::size_t k = 0; k < cnt; ++k) rec->descent_iters[k] = status[k] == MARS_RUN_SKIPPED ? 0 : iters[k];
+        if (rec->start_temp) std::copy(b->temp.begin(), b->temp.begin() + cnt, rec->start_temp);
+        // skipped slots carry zero records (runner.cpp:35-39)
+        for (std::size_t k = 0; k < cnt; ++k) {
+            if (status[k] != MARS_RUN_SKIPPED) continue;
+            if (rec->energy) rec->energy[k] = 0.0;
+            if (rec->cut) rec->cut[k] = 0.0;
+            if (rec->elapsed_seconds) rec->elapsed_seconds[k] = 0.0;
+            if (rec->spins) std::memset(rec->spins + k * p->n, 0, p->n);
+        }
+    }
+    if (best_index) *best_index = best < 0 ? -1 : b->first + best;
+    return MARS_OK;
+}
+
+void mars_batch_destroy(mars_batch_t* b) { delete b; }
+
+// runner.cpp:126-167 -- index-order aggregation; the all-failed batch is an error (153-155)
+int mars_aggregate(int64_t count, const uint8_t* status, const double* energy, const double* cut,
+                   const double* elapsed, double tol, double total_seconds, mars_stats_t* s) {
+    if (!s || (count > 0 && (!status || !energy || !cut)))
+        return fail(MARS_ERR_INPUT, "null argument");
+    *s = mars_stats_t{};
+    double cut_sum = 0.0, energy_sum = 0.0, run_seconds = 0.0;
+    std::int64_t best = -1;
+    for (std::int64_t i = 0; i < count; ++i) {
+        if (status[i] == MARS_RUN_SKIPPED) {
+            ++s->skipped_runs;
+            continue;
+        }
+        if (status[i] == MARS_RUN_DIVERGED) {
+            ++s->failed_runs;
+            continue;
+        }
+        ++s->completed_runs;
+        energy_sum += energy[i];
+        cut_sum += cut[i];
+        if (elapsed) run_seconds += elapsed[i];
+        if (best < 0 || energy[i] < s->best_energy) {
+            s->best_energy = energy[i];
+            best = i;
+        }
+        if (s->best_cut < cut[i] || s->completed_runs == 1) s->best_cut = cut[i];
+    }
+    s->best_index = best;
+    s->total_seconds = total_seconds;
+    if (s->completed_runs == 0)
+        return fail(MARS_ERR_ALL_FAILED, "batch failed: no run completed (" +
+                                             std::to_string(s->failed_runs) + " diverged, " +
+                                             std::to_string(s->skipped_runs) + " skipped)");
+    s->mean_energy = energy_sum / static_cast<double>(s->completed_runs);
+    s->mean_cut = cut_sum / static_cast<double>(s->completed_runs);
+    for (std::int64_t i = 0; i < count; ++i)
+        if (status[i] == MARS_RUN_OK && std::abs(energy[i] - s->best_energy) <= tol) ++s->hit_count;
+    s->success_probability = static_cast<double>(s->hit_count) / static_cast<double>(s->completed_runs);
+    s->mean_seconds_per_run = run_seconds / static_cast<double>(s->completed_runs);
+    return MARS_OK;
+}
+
+int mars_run_shard(mars_problem_t* p, const mars_params_t* prm, int64_t runs, uint64_t base_seed,
+                   int64_t first, int64_t count, mars_records_t* rec) {
+    mars_batch_t* b = nullptr;
+    if (int rc = mars_batch_create(p, prm, runs, base_seed, first, count, &b)) return rc;
+    int rc = mars_batch_upload(b);
+    if (!rc) rc = mars_batch_execute(b, nullptr);
+    if (!rc) rc = mars_batch_fetch(b, rec, nullptr, nullptr);
+    mars_batch_destroy(b);
+    return rc;
+}
+
+int mars_run_batch(mars_problem_t* p, const mars_params_t* prm, int64_t runs, uint64_t base_seed,
+                   mars_records_t* records, mars_stats_t* stats, int8_t* best_spins) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!p || !stats) return fail(MARS_ERR_INPUT, "null argument");
+    std::int64_t total = 0;
+    if (int rc = mars_run_count(prm, runs, &total)) return rc;   // InputError before any run
+    mars_batch_t* b = nullptr;
+    if (int rc = mars_batch_create(p, prm, runs, base_seed, 0, total, &b)) return rc;
+    std::vector<std::uint8_t> status(total);
+    std::vector<double> energy(total), cut(total), elapsed(total);
+    mars_records_t own{status.data(), energy.data(), cut.data(), nullptr, nullptr, elapsed.data(),
+                       records ? records->spins : nullptr};
+    if (records) {
+        own.start_temp = records->start_temp;
+        own.descent_iters = records->descent_iters;
+    }
+    std::int64_t best = -1;
+    int rc = mars_batch_upload(b);
+    if (!rc) rc = mars_batch_execute(b, nullptr);
+    if (!rc) rc = mars_batch_fetch(b, &own, &best, best_spins);
+    mars_batch_destroy(b);
+    if (rc) return rc;
+    if (records) {
+        if (records->status) std::copy(status.begin(), status.end(), records->status);
+        if (records->energy) std::copy(energy.begin(), energy.end(), records->energy);
+        if (records->cut) std::copy(cut.begin(), cut.end(), records->cut);
+        if (records->elapsed_seconds) std::copy(elapsed.begin(), elapsed.end(), records->elapsed_seconds);
+    }
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    rc = mars_aggregate(total, status.data(), energy.data(), cut.data(), elapsed.data(),
+                        p->integral ? 0.0 : 1e-9, secs, stats);
+    if (rc) return rc;
+    if (stats->best_index != best)
+        return fail(MARS_ERR_RUNTIME, "device best-of-R index " + std::to_string(best) +
+                                          " disagrees with the host aggregation " +
+                                          std::to_string(stats->best_index));
+    return MARS_OK;
+}
+
+// ------------------------------------------------------------ instance generators
+
+void mars_gen_sk_gaussian(int32_t n, uint64_t seed, double* J) {           // io.cpp:151-163
+    Stream r(seed);
+    std::memset(J, 0, sizeof(double) * static_cast<std::size_t>(n) * n);
+    for (int i = 0; i < n; ++i)
+        for (int k = i + 1; k < n; ++k) {
+            const double w = r.gaussian();
+            J[static_cast<std::size_t>(i) * n + k] = w;
+            J[static_cast<std::size_t>(k) * n + i] = w;
+        }
+}
+
+void mars_gen_sk_pm1(int32_t n, uint64_t seed, double* J) {
+    Stream r(seed);
+    std::memset(J, 0, sizeof(double) * static_cast<std::size_t>(n) * n);
+    for (int i = 0; i < n; ++i)
+        for (int k = i + 1; k < n; ++k) {
+            const double w = r.coin();
+            J[static_cast<std::size_t>(i) * n + k] = w;
+            J[static_cast<std::size_t>(k) * n + i] = w;
+        }
+}
+
+int64_t mars_gen_er(int32_t n, double prob, uint64_t seed, int32_t* u, int32_t* v, double* w) {
+    Stream r(seed);
+    std::int64_t m = 0;
+    for (int a = 0; a < n; ++a)
+        for (int b = a + 1; b < n; ++b)
+            if (r.open01() < prob) {
+                if (u) {
+                    u[m] = a;
+                    v[m] = b;
+                    w[m] = 1.0;
+                }
+                ++m;
+            }
+    return m;
+}
+
+int64_t mars_gen_ea(int32_t L, int32_t dims, uint64_t seed, int32_t* u, int32_t* v, double* w) {
+    Stream r(seed);
+    std::int64_t nsite = 1;
+    for (int d = 0; d < dims; ++d) nsite *= L;
+    std::int64_t m = 0;
+    for (std::int64_t i = 0; i < nsite; ++i) {
+        std::int64_t stride = 1;
+        for (int d = 0; d < dims; ++d) {
+            const std::int64_t c = (i / stride) % L;
+            const std::int64_t j = i + (c == L - 1 ? -static_cast<std::int64_t>(L - 1) * stride : stride);
+            const double wt = r.coin();
+            if (u) {
+                u[m] = static_cast<int32_t>(i);
+                v[m] = static_cast<int32_t>(j);
+                w[m] = wt;
+            }
+            ++m;
+            stride *= L;
+        }
+    }
+    return m;
+}
+
+}  // extern "C"

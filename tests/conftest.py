@@ -1,0 +1,65 @@
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (runs the sm_100a kernels)")
+    config.addinivalue_line("markers", "slow: long-running (full BASELINE-size workloads)")
+
+
+def _ensure_built():
+    """Build the oracle checkers and the native library if they are missing (CPU-only:
+    nvcc and gcc cross-compile here; on the GPU box the prebuilt files are used)."""
+    need_oracle = not os.path.exists(os.path.join(ROOT, "oracle", "libmars_oracle.so"))
+    if need_oracle and os.path.isdir("/root/reference/proj"):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle")], check=True,
+                       capture_output=True)
+    elif need_oracle:
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"),
+                        os.path.join(ROOT, "oracle", "libmars_oracle.so")], check=True,
+                       capture_output=True)
+    if not os.path.exists(os.path.join(ROOT, "paper_1907_05124_b200", "libmars_b200.so")):
+        from paper_1907_05124_b200._build import build
+        build()
+
+
+_ensure_built()
+
+
+def gpu_available() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def golden(name):
+    return np.load(os.path.join(GOLDEN, name + ".npz"))
+
+
+@pytest.fixture(scope="session")
+def port():
+    from oracle.oracle import Oracle
+    return Oracle("port")
+
+
+@pytest.fixture(scope="session")
+def ref():
+    from oracle.oracle import Oracle, LIBS
+    if not os.path.exists(LIBS["ref"]):
+        pytest.skip("oracle/_ref not built (reference sources absent on this machine)")
+    return Oracle("ref")
+
+
+def unpack_spins(packed, n):
+    return np.where(np.unpackbits(packed, axis=-1)[..., :n] > 0, 1, -1).astype(np.int8)
