@@ -18,20 +18,22 @@ struct RelaxArgs {
     int np;            // padded spins (multiple of the kernel's block size)
     // dense couplings, fp32 row-major [np][np], zero padded
     const float* J32;
-    // CSR couplings (neighbours sorted ascending, model.cpp:116-127)
+    // CSR couplings (neighbours sorted ascending, model.cpp:116-127), fp64 weights
     const int* off;
     const int* idx;
-    const float* w32;
-    const float* h32;          // [n] external field, or nullptr
+    const double* w64;
+    const float* h32;          // [n] external field, or nullptr (fp32 kernels)
+    const double* h64;         // [n] external field, or nullptr (fp64 kernels)
     // the runs of this launch
     int queue_len;             // descents to run
     const int* order;          // [queue_len] local run index, processing order
-    const float* s0;           // [count][n] initial states (fp32 of the fp64 draws)
+    const float* s0;           // [count][n] initial states, fp32 (dense fp32 kernels)
+    const void* s0_64;         // [count][n] initial states, fp64 as drawn (fp64 kernels)
     const double* start_temp;  // [count]
     double c_step, d_min;
     long long sweep_cap;
     // scratch
-    float* work;               // per-CTA slot state, kernel-specific layout
+    void* work;                // per-CTA slot state, kernel-specific layout
     int* queue_head;           // atomic counter, zero before launch
     // per-run outputs (local run index)
     std::uint8_t* status;
@@ -69,11 +71,11 @@ struct BestArgs {
 cudaError_t launch_relax_dense_simt(const RelaxArgs& a, int grid, cudaStream_t st);
 int relax_dense_simt_slots_per_cta();
 int relax_dense_simt_block();
-std::size_t relax_dense_simt_work_floats(int np);
+std::size_t relax_dense_simt_work_bytes(int np);
 
 cudaError_t launch_relax_csr(const RelaxArgs& a, int grid, cudaStream_t st);
 int relax_csr_slots_per_cta();
-std::size_t relax_csr_work_floats(int np);
+std::size_t relax_csr_work_bytes(int np);
 
 cudaError_t launch_energy(const EnergyArgs& a, cudaStream_t st);
 cudaError_t launch_best(const BestArgs& a, int grid, cudaStream_t st);

@@ -120,10 +120,13 @@ struct mars_problem {
     // device copies
     float* dJ32 = nullptr;          // [np][np] fp32, zero padded (dense kernels)
     double* dJ64 = nullptr;         // [n][n]   fp64 (exact energy, dense storage)
-    int* dOff = nullptr;
+    int* dOff = nullptr;            // CSR of the reference storage (exact energy)
     int* dIdx = nullptr;
-    float* dW32 = nullptr;
     double* dW64 = nullptr;
+    int* rOff = nullptr;            // CSR the relaxation kernel walks (aliases dOff/... for
+    int* rIdx = nullptr;            //  adjacency storage; built from the nonzeros otherwise)
+    double* rW64 = nullptr;
+    bool r_owned = false;
     float* dH32 = nullptr;
     double* dH64 = nullptr;
 
@@ -133,8 +136,12 @@ struct mars_problem {
         cudaFree(dJ64);
         cudaFree(dOff);
         cudaFree(dIdx);
-        cudaFree(dW32);
         cudaFree(dW64);
+        if (r_owned) {
+            cudaFree(rOff);
+            cudaFree(rIdx);
+            cudaFree(rW64);
+        }
         cudaFree(dH32);
         cudaFree(dH64);
         if (stream) cudaStreamDestroy(stream);
@@ -176,8 +183,16 @@ int upload(T** dst, const T* src, std::size_t count) {
     return MARS_OK;
 }
 
+// Instances whose nonzero density is below this run on the fp64 CSR kernel even when the
+// reference stores them dense (e.g. the G1-shape 6% graph): its summation over the sorted
+// nonzeros is bit-identical to the dense row_dot (zeros add nothing), and it is cheaper.
+constexpr double kCsrDensity = 0.10;
+
 int resolve_kernel(mars_problem* p, int requested) {
-    if (requested == MARS_KERNEL_AUTO) return p->dense ? MARS_KERNEL_DENSE_SIMT : MARS_KERNEL_CSR;
+    if (requested == MARS_KERNEL_AUTO) {
+        const double density = static_cast<double>(p->nnz) / (static_cast<double>(p->n) * p->n);
+        return (!p->dense || density < kCsrDensity) ? MARS_KERNEL_CSR : MARS_KERNEL_DENSE_SIMT;
+    }
     if (requested == MARS_KERNEL_DENSE_SIMT || requested == MARS_KERNEL_CSR) return requested;
     return -1;
 }
@@ -223,38 +238,40 @@ int build_device_store(mars_problem* p) {
         if (int rc = upload(&p->dJ32, j32.data(), j32.size())) return rc;
     } else {
         p->np = n;
-        std::vector<int> off, idx;
-        std::vector<float> w32;
         if (p->dense) {  // CSR view of a dense store, ascending columns (row_dot order minus zeros)
-            off.assign(n + 1, 0);
+            std::vector<int> off(n + 1, 0), idx;
+            std::vector<double> w64;
             for (int i = 0; i < n; ++i) {
                 for (int j = 0; j < n; ++j) {
                     const double w = p->J[static_cast<std::size_t>(i) * n + j];
                     if (w != 0.0) {
                         idx.push_back(j);
-                        w32.push_back(static_cast<float>(w));
+                        w64.push_back(w);
                     }
                 }
                 off[i + 1] = static_cast<int>(idx.size());
             }
-            if (int rc = upload(&p->dOff, off.data(), off.size())) return rc;
-            if (int rc = upload(&p->dIdx, idx.data(), idx.size())) return rc;
+            p->r_owned = true;
+            if (int rc = upload(&p->rOff, off.data(), off.size())) return rc;
+            if (int rc = upload(&p->rIdx, idx.data(), idx.size())) return rc;
+            if (int rc = upload(&p->rW64, w64.data(), w64.size())) return rc;
         } else {
-            w32.assign(p->wt.begin(), p->wt.end());
+            p->rOff = p->dOff;
+            p->rIdx = p->dIdx;
+            p->rW64 = p->dW64;
         }
-        if (int rc = upload(&p->dW32, w32.data(), w32.size())) return rc;
     }
     return MARS_OK;
 }
 
 int finish_problem(mars_problem* p, int device, int kernel, mars_problem_t** out) {
     p->device = device;
+    finalize_metadata(p);
     p->kernel = resolve_kernel(p, kernel);
     if (p->kernel < 0) {
         delete p;
         return fail(MARS_ERR_INPUT, "unknown kernel selection " + std::to_string(kernel));
     }
-    finalize_metadata(p);
     if (int rc = build_device_store(p)) {
         delete p;
         return rc;
@@ -279,16 +296,17 @@ struct mars_batch {
     // host plan
     std::vector<std::uint8_t> skipped;
     std::vector<double> temp;
-    float* h_s0 = nullptr;          // pinned [count][n]
+    void* h_s0 = nullptr;           // pinned [count][n], fp32 or fp64 per kernel
+    std::size_t s0_elem = 4;
     int* h_order = nullptr;         // pinned [count]
     double* h_temp = nullptr;       // pinned [count]
     std::uint8_t* h_status = nullptr;  // pinned [count]
     // device
-    float* d_s0 = nullptr;
+    void* d_s0 = nullptr;
     double* d_temp = nullptr;
     int* d_order = nullptr;
     float* d_work = nullptr;
-    std::size_t work_floats = 0;
+    std::size_t work_bytes = 0;
     int* d_queue = nullptr;
     std::uint8_t* d_status = nullptr;
     long long* d_iters = nullptr;
@@ -335,11 +353,12 @@ int batch_alloc(mars_batch* b) {
     const std::size_t cnt = static_cast<std::size_t>(std::max<std::int64_t>(b->count, 1));
     const std::size_t n = static_cast<std::size_t>(p->n);
     CUDA_TRY(cudaSetDevice(p->device));
-    CUDA_TRY(cudaMallocHost(&b->h_s0, cnt * n * sizeof(float)));
+    b->s0_elem = p->kernel == MARS_KERNEL_CSR ? sizeof(double) : sizeof(float);
+    CUDA_TRY(cudaMallocHost(&b->h_s0, cnt * n * b->s0_elem));
     CUDA_TRY(cudaMallocHost(&b->h_order, cnt * sizeof(int)));
     CUDA_TRY(cudaMallocHost(&b->h_temp, cnt * sizeof(double)));
     CUDA_TRY(cudaMallocHost(&b->h_status, cnt));
-    CUDA_TRY(cudaMalloc(&b->d_s0, cnt * n * sizeof(float)));
+    CUDA_TRY(cudaMalloc(&b->d_s0, cnt * n * b->s0_elem));
     CUDA_TRY(cudaMalloc(&b->d_temp, cnt * sizeof(double)));
     CUDA_TRY(cudaMalloc(&b->d_order, cnt * sizeof(int)));
     CUDA_TRY(cudaMalloc(&b->d_queue, sizeof(int)));
@@ -383,16 +402,16 @@ int batch_alloc(mars_batch* b) {
     int max_grid = p->num_sms;
     if (p->kernel == MARS_KERNEL_DENSE_SIMT) {
         tm = relax_dense_simt_slots_per_cta();
-        per_cta = relax_dense_simt_work_floats(p->np);
+        per_cta = relax_dense_simt_work_bytes(p->np);
     } else {
         tm = relax_csr_slots_per_cta();
-        per_cta = relax_csr_work_floats(p->np);
+        per_cta = relax_csr_work_bytes(p->np);
         max_grid = 8 * p->num_sms;
     }
     b->grid = std::max(1, std::min(max_grid, (b->queue_len + tm - 1) / tm));
     b->slots = b->grid * tm;
-    b->work_floats = per_cta * b->grid;
-    CUDA_TRY(cudaMalloc(&b->d_work, b->work_floats * sizeof(float)));
+    b->work_bytes = per_cta * b->grid;
+    CUDA_TRY(cudaMalloc(&b->d_work, b->work_bytes));
     return MARS_OK;
 }
 
@@ -602,13 +621,18 @@ int mars_batch_upload(mars_batch_t* b) {
         for (std::int64_t k = lo; k < hi; ++k) {
             if (b->skipped[k]) continue;
             Stream r(sub_seed(b->base_seed, static_cast<std::uint64_t>(b->first + k)));
-            float* row = b->h_s0 + static_cast<std::size_t>(k) * n;
-            for (int i = 0; i < n; ++i) row[i] = static_cast<float>(r.open_sym());
+            if (b->s0_elem == sizeof(double)) {
+                double* row = static_cast<double*>(b->h_s0) + static_cast<std::size_t>(k) * n;
+                for (int i = 0; i < n; ++i) row[i] = r.open_sym();
+            } else {
+                float* row = static_cast<float*>(b->h_s0) + static_cast<std::size_t>(k) * n;
+                for (int i = 0; i < n; ++i) row[i] = static_cast<float>(r.open_sym());
+            }
         }
     });
     CUDA_TRY(cudaSetDevice(p->device));
     const std::size_t cnt = static_cast<std::size_t>(b->count);
-    CUDA_TRY(cudaMemcpyAsync(b->d_s0, b->h_s0, cnt * n * sizeof(float), cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(b->d_s0, b->h_s0, cnt * n * b->s0_elem, cudaMemcpyHostToDevice, p->stream));
     CUDA_TRY(cudaMemcpyAsync(b->d_temp, b->h_temp, cnt * sizeof(double), cudaMemcpyHostToDevice, p->stream));
     CUDA_TRY(cudaMemcpyAsync(b->d_order, b->h_order, std::max(b->queue_len, 1) * sizeof(int),
                              cudaMemcpyHostToDevice, p->stream));
@@ -628,18 +652,20 @@ int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
     if (b->executed)  // re-execution: restore the pending statuses
         CUDA_TRY(cudaMemcpyAsync(b->d_status, b->h_status, b->count, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemsetAsync(b->d_queue, 0, sizeof(int), st));
-    CUDA_TRY(cudaMemsetAsync(b->d_work, 0, b->work_floats * sizeof(float), st));
+    CUDA_TRY(cudaMemsetAsync(b->d_work, 0, b->work_bytes, st));
     RelaxArgs ra{};
     ra.n = p->n;
     ra.np = p->np;
     ra.J32 = p->dJ32;
-    ra.off = p->dOff;
-    ra.idx = p->dIdx;
-    ra.w32 = p->dW32;
+    ra.off = p->rOff;
+    ra.idx = p->rIdx;
+    ra.w64 = p->rW64;
     ra.h32 = p->dH32;
+    ra.h64 = p->dH64;
     ra.queue_len = b->queue_len;
     ra.order = b->d_order;
-    ra.s0 = b->d_s0;
+    ra.s0 = static_cast<const float*>(b->d_s0);
+    ra.s0_64 = b->d_s0;
     ra.start_temp = b->d_temp;
     ra.c_step = b->prm.c_step;
     ra.d_min = b->prm.d_min;

@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(NT, 1) relax_dense_simt_kernel(RelaxArgs a) {
     const int tid = threadIdx.x;
     const int n = a.n, np = a.np;
     const int nb = np / TB, nk = np / KC;
-    float* W = a.work + static_cast<size_t>(blockIdx.x) * np * TM;
+    float* W = static_cast<float*>(a.work) + static_cast<size_t>(blockIdx.x) * np * TM;
     const int tx = tid & 15, ty = tid >> 4;
     const int warp = tid >> 5, lane = tid & 31;
 
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(NT, 1) relax_dense_simt_kernel(RelaxArgs a) {
 
 int relax_dense_simt_slots_per_cta() { return TM; }
 int relax_dense_simt_block() { return TB; }
-std::size_t relax_dense_simt_work_floats(int np) { return static_cast<std::size_t>(np) * TM; }
+std::size_t relax_dense_simt_work_bytes(int np) { return static_cast<std::size_t>(np) * TM * sizeof(float); }
 
 cudaError_t launch_relax_dense_simt(const RelaxArgs& a, int grid, cudaStream_t st) {
     const int smem = static_cast<int>(sizeof(Smem));

