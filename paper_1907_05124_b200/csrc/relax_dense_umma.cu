@@ -1,0 +1,374 @@
+// relax_dense_umma.cu -- persistent blocked Gauss-Seidel MARS relaxation on tcgen05 tensor
+// cores (sm_100a): TMA-fed UMMA field GEMM into TMEM + fused Gauss-Seidel epilogue.
+//
+// Replaces, for a tile of TM = 128 concurrent descents per CTA (one TMEM lane per run):
+//   mars_relax_sweep        solvers.cpp:150-161  (in-place ascending-index Gauss-Seidel)
+//   IsingProblem::row_dot   model.cpp:141-146    (dense row dot product)
+//   tanh_trial              solvers.cpp:145-148
+//   relax_to_fixed_point    solvers.cpp:163-176  and the mars_descent level loop 178-200
+//   run_batch_with's queue  runner.cpp:95-115    (slots refill from an atomic run queue)
+//
+// Algorithm (left-looking blocked Gauss-Seidel).  For spin block b (TB spins) the fields of
+// all 128 runs are one GEMM over the whole current state,
+//     Phi[r][i] = sum_j S[r][j] * J[j][b*TB + i]      (runs on TMEM lanes, spins on columns)
+// where S holds this sweep's new values for j < b*TB and the previous sweep's for j >= b*TB.
+// The epilogue (one thread per run) then walks the block in ascending order adding the
+// in-block corrections J[k][i]*(s_i_new - s_i_old) for k > i -- exactly the reference's
+// update order; only the summation order/precision differs.
+//
+// Precision ("fp32-accurate split"): the state is kept as an fp16 pair s = hi + lo (22-23
+// significant bits) and J as J_hi + J_lo, and the field is J_hi*S_hi + J_hi*S_lo + J_lo*S_hi
+// accumulated in fp32 (J_lo*S_lo < 2^-22 relative is dropped).  Integer couplings
+// (|J| <= 2048) are exact in J_hi, so the J_lo product is skipped (JLO = false).
+//
+// Pipelining.  GEMM(b) consumes its K chunks starting at block b and ending with block
+// b-1, so it runs concurrently with the epilogue of block b-1 and only its last TB/KC
+// chunks wait for that epilogue's state write-back; two TMEM accumulators ping-pong.
+// A finished slot is refilled without stalling the pipeline: for one "loading" sweep the
+// epilogue streams the old run's final spins out and the new run's initial state in, block
+// by block, in Gauss-Seidel order, so every GEMM always reads a consistent state.
+//
+// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer,
+// warps 2..5 = epilogue (warp w accesses TMEM lanes 32*(w%4) .. +31).
+//
+// Global layout: state planes S_hi/S_lo [grid*TM][np] fp16 (row per slot, K-major for
+// UMMA), couplings J_hi/J_lo [np][np] fp16 (J symmetric, so row i of J is column i: the
+// K-major B operand of block b is the row block J[b*TB .. b*TB+TB)[*]), J32 [np][np] fp32
+// for the epilogue's diagonal block.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+#include "slot.cuh"
+#include "umma.cuh"
+
+namespace marsb200 {
+namespace {
+
+using namespace umma;
+
+constexpr int TM = 128;      // runs per CTA = TMEM lanes = UMMA M
+constexpr int TB = 128;      // spins per Gauss-Seidel block = UMMA N
+constexpr int KC = 64;       // K per pipeline stage (one 128-byte swizzle atom of fp16)
+constexpr int CPB = TB / KC; // chunks per block
+constexpr int STAGES = 2;
+constexpr int NT = 192;
+constexpr int EPI0 = 2;      // first epilogue warp
+constexpr std::uint32_t TILE_A = TM * KC * 2;   // 16 KB
+constexpr std::uint32_t TILE_J = TB * KC * 2;   // 16 KB
+constexpr std::uint32_t STAGE_BYTES = 2 * TILE_A + 2 * TILE_J;
+
+enum : int { kIdle = 0, kActive = 1, kLoading = 2, kDrain = 3 };
+
+struct __align__(8) Ctl {
+    std::uint64_t full[STAGES];
+    std::uint64_t empty[STAGES];
+    std::uint64_t tmem_full[2];
+    std::uint64_t tmem_empty[2];
+    std::uint64_t chunk_ready;
+    std::uint64_t mma_done;
+    std::uint32_t tmem_base;
+    volatile std::uint32_t stop;
+    volatile std::uint32_t poison_it;
+};
+
+// dynamic smem: [stages: A_hi A_lo J_hi J_lo] [Jd fp32 TB*TB] [Ctl]
+constexpr std::uint32_t SMEM_STAGES = STAGES * STAGE_BYTES;
+constexpr std::uint32_t SMEM_JD = TB * TB * 4;
+constexpr std::uint32_t SMEM_TOTAL = SMEM_STAGES + SMEM_JD + sizeof(Ctl) + 1024;
+
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+
+__device__ __forceinline__ bool epi_any(bool v) {
+    std::uint32_t r;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t"
+        "setp.ne.u32 p, %1, 0;\n\t"
+        "barrier.cta.red.or.pred q, 1, 128, p;\n\t"
+        "selp.u32 %0, 1, 0, q;\n\t}\n"
+        : "=r"(r)
+        : "r"(static_cast<std::uint32_t>(v))
+        : "memory");
+    return r != 0;
+}
+
+struct UmmaParams {
+    const __half* s_hi;      // state planes (generic pointers for the epilogue)
+    __half* s_hi_w;
+    __half* s_lo_w;
+    int nb;                  // blocks per sweep = np / TB
+};
+
+__device__ __forceinline__ void split16(float v, __half& hi, __half& lo, float& back) {
+    hi = __float2half_rn(v);
+    lo = __float2half_rn(v - __half2float(hi));
+    back = __half2float(hi) + __half2float(lo);
+}
+
+template <bool JLO>
+__global__ void __launch_bounds__(NT, 1)
+relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUtensorMap tm_shi,
+                        const __grid_constant__ CUtensorMap tm_slo,
+                        const __grid_constant__ CUtensorMap tm_jhi,
+                        const __grid_constant__ CUtensorMap tm_jlo) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* base = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+    float* Jd = reinterpret_cast<float*>(base + SMEM_STAGES);
+    Ctl& ctl = *reinterpret_cast<Ctl*>(base + SMEM_STAGES + SMEM_JD);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int np = a.np, n = a.n, nb = up.nb, nk = np / KC;
+    const int row0 = blockIdx.x * TM;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&ctl.full[s], 1);
+            mbar_init(&ctl.empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&ctl.tmem_full[s], 1);
+            mbar_init(&ctl.tmem_empty[s], TM);
+        }
+        mbar_init(&ctl.chunk_ready, TM);
+        mbar_init(&ctl.mma_done, 1);
+        ctl.stop = 0;
+        ctl.poison_it = 0xFFFFFFFFu;
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc(&ctl.tmem_base, 2 * TB);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const std::uint32_t tmem = ctl.tmem_base;
+
+    if (warp == 0) {
+        // ================================================================ TMA producer
+        if (lane == 0) {
+            tma_prefetch_desc(&tm_shi);
+            tma_prefetch_desc(&tm_slo);
+            tma_prefetch_desc(&tm_jhi);
+            if (JLO) tma_prefetch_desc(&tm_jlo);
+            std::uint32_t g = 0, it = 0;
+            for (;;) {
+                for (int b = 0; b < nb; ++b, ++g) {
+                    for (int j = 0; j < nk; ++j, ++it) {
+                        if (j == nk - CPB && g > 0) {
+                            // the last chunks of GEMM(b) are block b-1: wait for its update
+                            mbar_wait(&ctl.chunk_ready, (g - 1) & 1);
+                            if (ctl.stop) {
+                                const int s = it % STAGES;
+                                mbar_wait(&ctl.empty[s], ((it / STAGES) & 1) ^ 1);
+                                ctl.poison_it = it;
+                                mbar_arrive(&ctl.full[s]);
+                                goto producer_done;
+                            }
+                        }
+                        const int s = it % STAGES;
+                        const int c = (b * CPB + j) % nk;
+                        mbar_wait(&ctl.empty[s], ((it / STAGES) & 1) ^ 1);
+                        unsigned char* st = base + s * STAGE_BYTES;
+                        mbar_arrive_expect_tx(&ctl.full[s], JLO ? STAGE_BYTES : STAGE_BYTES - TILE_J);
+                        tma_load_2d(st, &tm_shi, &ctl.full[s], c * KC, row0);
+                        tma_load_2d(st + TILE_A, &tm_slo, &ctl.full[s], c * KC, row0);
+                        tma_load_2d(st + 2 * TILE_A, &tm_jhi, &ctl.full[s], c * KC, b * TB);
+                        if (JLO) tma_load_2d(st + 2 * TILE_A + TILE_J, &tm_jlo, &ctl.full[s], c * KC, b * TB);
+                    }
+                }
+            }
+        producer_done:;
+        }
+    } else if (warp == 1) {
+        // ================================================================ MMA issuer
+        if (lane == 0) {
+            constexpr std::uint32_t idesc = idesc_f16(TM, TB, 0);
+            std::uint32_t g = 0, it = 0;
+            for (;;) {
+                for (int b = 0; b < nb; ++b, ++g) {
+                    const int buf = g & 1;
+                    mbar_wait(&ctl.tmem_empty[buf], ((g >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                    const std::uint32_t d = tmem + buf * TB;
+                    for (int j = 0; j < nk; ++j, ++it) {
+                        const int s = it % STAGES;
+                        mbar_wait(&ctl.full[s], (it / STAGES) & 1);
+                        if (ctl.poison_it == it) goto mma_done;
+                        tc_fence_after();
+                        const std::uint32_t st = smem_u32(base + s * STAGE_BYTES);
+#pragma unroll
+                        for (int kk = 0; kk < KC / 16; ++kk) {
+                            const std::uint64_t ahi = desc_k_sw128(st + kk * 32);
+                            const std::uint64_t alo = desc_k_sw128(st + TILE_A + kk * 32);
+                            const std::uint64_t jhi = desc_k_sw128(st + 2 * TILE_A + kk * 32);
+                            mma_f16_ss(d, ahi, jhi, idesc, (j | kk) != 0);
+                            mma_f16_ss(d, alo, jhi, idesc, 1);
+                            if (JLO) {
+                                const std::uint64_t jlo = desc_k_sw128(st + 2 * TILE_A + TILE_J + kk * 32);
+                                mma_f16_ss(d, ahi, jlo, idesc, 1);
+                            }
+                        }
+                        mma_commit(&ctl.empty[s]);
+                    }
+                    mma_commit(&ctl.tmem_full[buf]);
+                }
+            }
+        mma_done:
+            mma_commit(&ctl.mma_done);
+            mbar_wait(&ctl.mma_done, 0);
+        }
+        __syncwarp();
+    } else {
+        // ================================================================ epilogue
+        const int q = warp & 3;                 // TMEM lane quarter
+        const int r = q * 32 + lane;            // slot = TMEM lane
+        const int et = threadIdx.x - EPI0 * 32; // 0..127 for cooperative loads
+        __half* hi_row = up.s_hi_w + static_cast<size_t>(row0 + r) * np;
+        __half* lo_row = up.s_lo_w + static_cast<size_t>(row0 + r) * np;
+
+        Slot slot;
+        slot.run = -1;
+        int mode = kIdle, old_run = -1, new_run = claim_run(a);
+        if (new_run >= 0) mode = kLoading;
+        std::uint32_t g = 0;
+
+        for (;;) {
+            const bool active = mode == kActive;
+            const bool quench = active && slot_quench(slot);
+            const float Tf = static_cast<float>(slot.T);
+            float dmax = 0.0f;
+            for (int b = 0; b < nb; ++b, ++g) {
+                const int b0 = b * TB;
+                const int lim = min(TB, n - b0);
+                // diagonal block J[b0+i][b0+k] -> smem (after everyone finished the last one)
+                epi_sync();
+                {
+                    const float4* src = reinterpret_cast<const float4*>(a.J32);
+#pragma unroll 4
+                    for (int f = et; f < TB * TB / 4; f += TM) {
+                        const int i = f / (TB / 4), k4 = f % (TB / 4);
+                        reinterpret_cast<float4*>(Jd)[f] =
+                            __ldg(src + (static_cast<size_t>(b0 + i) * np + b0) / 4 + k4);
+                    }
+                }
+                epi_sync();
+                const int buf = g & 1;
+                mbar_wait(&ctl.tmem_full[buf], (g >> 1) & 1);
+                tc_fence_after();
+                float phi[TB];
+#pragma unroll
+                for (int c = 0; c < TB / 32; ++c) {
+                    float v[32];
+                    tmem_ld32(tmem + (static_cast<std::uint32_t>(q * 32) << 16) + buf * TB + c * 32, v);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) phi[c * 32 + j] = v[j];
+                }
+                tmem_ld_wait();
+                tc_fence_before();
+                mbar_arrive(&ctl.tmem_empty[buf]);
+
+                if (active) {
+                    // ---- in-block Gauss-Seidel correction, ascending spin order
+                    __half hbuf[TB], lbuf[TB];
+#pragma unroll
+                    for (int v = 0; v < TB / 8; ++v) {
+                        *reinterpret_cast<uint4*>(&hbuf[v * 8]) = *reinterpret_cast<const uint4*>(hi_row + b0 + v * 8);
+                        *reinterpret_cast<uint4*>(&lbuf[v * 8]) = *reinterpret_cast<const uint4*>(lo_row + b0 + v * 8);
+                    }
+#pragma unroll
+                    for (int i = 0; i < TB; ++i) {
+                        if (i < lim) {
+                            const float x = phi[i] + (a.h32 ? __ldg(a.h32 + b0 + i) : 0.0f);
+                            const float trial = tanh_trial(x, Tf, quench);
+                            float snew;
+                            const float sold = __half2float(hbuf[i]) + __half2float(lbuf[i]);
+                            split16(trial, hbuf[i], lbuf[i], snew);
+                            const float delta = snew - sold;
+                            dmax = fmaxf(dmax, fabsf(delta));
+#pragma unroll
+                            for (int k = i + 1; k < TB; ++k) phi[k] = fmaf(Jd[i * TB + k], delta, phi[k]);
+                        }
+                    }
+#pragma unroll
+                    for (int v = 0; v < TB / 8; ++v) {
+                        *reinterpret_cast<uint4*>(hi_row + b0 + v * 8) = *reinterpret_cast<const uint4*>(&hbuf[v * 8]);
+                        *reinterpret_cast<uint4*>(lo_row + b0 + v * 8) = *reinterpret_cast<const uint4*>(&lbuf[v * 8]);
+                    }
+                } else if (mode == kLoading || mode == kDrain) {
+                    // ---- slot turnover, block by block: old run's spins out, new run's s0 in
+                    if (old_run >= 0) {
+                        std::int8_t* out = a.spins + static_cast<size_t>(old_run) * n + b0;
+                        for (int i = 0; i < lim; ++i) {                   // round_spins (model.cpp:245)
+                            const float s = __half2float(hi_row[b0 + i]) + __half2float(lo_row[b0 + i]);
+                            out[i] = s < 0.0f ? -1 : 1;
+                        }
+                    }
+                    if (mode == kLoading) {
+                        const float* src = a.s0 + static_cast<size_t>(new_run) * n + b0;
+                        for (int i = 0; i < TB; ++i) {
+                            __half h, l;
+                            float back;
+                            split16(i < lim ? src[i] : 0.0f, h, l, back);
+                            hi_row[b0 + i] = h;
+                            lo_row[b0 + i] = l;
+                        }
+                    }
+                }
+                if (b == nb - 1) {
+                    // ---- end of sweep: annealing state machine (solvers.cpp:178-200)
+                    if (active) {
+                        const int code = slot_after_sweep(slot, dmax, a);
+                        if (code != kSlotContinue) {
+                            slot_finish(slot, code, a);
+                            old_run = slot.run;
+                            new_run = claim_run(a);
+                            mode = new_run >= 0 ? kLoading : kDrain;
+                        }
+                    } else if (mode == kLoading) {
+                        slot_start(slot, new_run, a);
+                        mode = kActive;
+                        old_run = -1;
+                    } else if (mode == kDrain) {
+                        mode = kIdle;
+                        old_run = -1;
+                    }
+                    const bool more = epi_any(mode != kIdle);
+                    if (!more && et == 0) ctl.stop = 1;
+                    fence_proxy_async_global();
+                    mbar_arrive(&ctl.chunk_ready);
+                    if (!more) goto epilogue_done;
+                } else {
+                    fence_proxy_async_global();
+                    mbar_arrive(&ctl.chunk_ready);
+                }
+            }
+        }
+    epilogue_done:;
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc(tmem, 2 * TB);
+}
+
+}  // namespace
+
+int relax_dense_umma_slots_per_cta() { return TM; }
+int relax_dense_umma_block() { return TB; }
+std::size_t relax_dense_umma_plane_rows(int grid) { return static_cast<std::size_t>(grid) * TM; }
+
+cudaError_t launch_relax_dense_umma(const RelaxArgs& a, const UmmaLaunch& u, int grid, cudaStream_t st) {
+    UmmaParams up{u.s_hi, u.s_hi, u.s_lo, a.np / TB};
+    cudaError_t e;
+    if (u.jlo) {
+        e = cudaFuncSetAttribute(relax_dense_umma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
+        if (e != cudaSuccess) return e;
+        relax_dense_umma_kernel<true><<<grid, NT, SMEM_TOTAL, st>>>(a, up, u.tm_shi, u.tm_slo, u.tm_jhi, u.tm_jlo);
+    } else {
+        e = cudaFuncSetAttribute(relax_dense_umma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
+        if (e != cudaSuccess) return e;
+        relax_dense_umma_kernel<false><<<grid, NT, SMEM_TOTAL, st>>>(a, up, u.tm_shi, u.tm_slo, u.tm_jhi, u.tm_jlo);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace marsb200

@@ -30,6 +30,18 @@ def _ensure_built():
     if not os.path.exists(os.path.join(ROOT, "paper_1907_05124_b200", "libmars_b200.so")):
         from paper_1907_05124_b200._build import build
         build()
+    probe = os.path.join(ROOT, "tests", "cuda", "libumma_probe.so")
+    if not os.path.exists(probe):
+        build_probe()
+
+
+def build_probe():
+    """TEST-ONLY one-CTA GEMM through the product's tcgen05/TMA helpers (tests/cuda)."""
+    src = os.path.join(ROOT, "tests", "cuda", "umma_probe.cu")
+    out = os.path.join(ROOT, "tests", "cuda", "libumma_probe.so")
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2", "-std=c++17",
+                    "-Xcompiler", "-fPIC", "-shared", "-o", out, src], check=True,
+                   capture_output=True)
 
 
 _ensure_built()
