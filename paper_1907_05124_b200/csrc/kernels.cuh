@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 namespace marsb200 {
@@ -72,6 +74,19 @@ cudaError_t launch_relax_dense_simt(const RelaxArgs& a, int grid, cudaStream_t s
 int relax_dense_simt_slots_per_cta();
 int relax_dense_simt_block();
 std::size_t relax_dense_simt_work_bytes(int np);
+
+// tcgen05 dense kernel: TMA maps over the fp16 state planes ([grid*128][np], per batch)
+// and the fp16 coupling planes ([np][np], per problem).
+struct UmmaLaunch {
+    CUtensorMap tm_shi, tm_slo, tm_jhi, tm_jlo;
+    __half* s_hi;
+    __half* s_lo;
+    bool jlo;   // Gaussian couplings need the J_lo product; integer ones are exact in J_hi
+};
+cudaError_t launch_relax_dense_umma(const RelaxArgs& a, const UmmaLaunch& u, int grid, cudaStream_t st);
+int relax_dense_umma_slots_per_cta();
+int relax_dense_umma_block();
+std::size_t relax_dense_umma_plane_rows(int grid);
 
 cudaError_t launch_relax_csr(const RelaxArgs& a, int grid, cudaStream_t st);
 int relax_csr_slots_per_cta();

@@ -22,6 +22,7 @@
 #include "../../include/mars_b200.h"
 #include "kernels.cuh"
 #include "rng.hpp"
+#include "tma_host.hpp"
 
 using namespace marsb200;
 
@@ -129,8 +130,14 @@ struct mars_problem {
     bool r_owned = false;
     float* dH32 = nullptr;
     double* dH64 = nullptr;
+    __half* dJhi = nullptr;         // [np][np] fp16 split of J (tcgen05 kernel)
+    __half* dJlo = nullptr;
+    bool jlo = true;                // J_lo nonzero somewhere (non-integer couplings)
+    CUtensorMap tm_jhi{}, tm_jlo{};
 
     ~mars_problem() {
+        cudaFree(dJhi);
+        cudaFree(dJlo);
         cudaSetDevice(device);
         cudaFree(dJ32);
         cudaFree(dJ64);
@@ -193,7 +200,9 @@ int resolve_kernel(mars_problem* p, int requested) {
         const double density = static_cast<double>(p->nnz) / (static_cast<double>(p->n) * p->n);
         return (!p->dense || density < kCsrDensity) ? MARS_KERNEL_CSR : MARS_KERNEL_DENSE_SIMT;
     }
-    if (requested == MARS_KERNEL_DENSE_SIMT || requested == MARS_KERNEL_CSR) return requested;
+    if (requested == MARS_KERNEL_DENSE_SIMT || requested == MARS_KERNEL_CSR ||
+        requested == MARS_KERNEL_DENSE_UMMA)
+        return requested;
     return -1;
 }
 
@@ -222,8 +231,9 @@ int build_device_store(mars_problem* p) {
         if (int rc = upload(&p->dH32, h32.data(), h32.size())) return rc;
     }
     // relaxation operands
-    if (p->kernel == MARS_KERNEL_DENSE_SIMT) {
-        p->np = round_up(n, relax_dense_simt_block());
+    if (p->kernel == MARS_KERNEL_DENSE_SIMT || p->kernel == MARS_KERNEL_DENSE_UMMA) {
+        p->np = round_up(n, p->kernel == MARS_KERNEL_DENSE_UMMA ? relax_dense_umma_block()
+                                                                 : relax_dense_simt_block());
         std::vector<float> j32(static_cast<std::size_t>(p->np) * p->np, 0.0f);
         if (p->dense) {
             for (int i = 0; i < n; ++i)
@@ -236,6 +246,26 @@ int build_device_store(mars_problem* p) {
                     j32[static_cast<std::size_t>(i) * p->np + p->idx[k]] += static_cast<float>(p->wt[k]);
         }
         if (int rc = upload(&p->dJ32, j32.data(), j32.size())) return rc;
+        if (p->kernel == MARS_KERNEL_DENSE_UMMA) {
+            // fp16 split J = J_hi + J_lo (the tensor-core operand planes)
+            std::vector<__half> jh(j32.size()), jl(j32.size());
+            p->jlo = false;
+            for (std::size_t k = 0; k < j32.size(); ++k) {
+                const int i = static_cast<int>(k / p->np), j = static_cast<int>(k % p->np);
+                const double w = (i < n && j < n)
+                                     ? (p->dense ? p->J[static_cast<std::size_t>(i) * n + j] : static_cast<double>(j32[k]))
+                                     : 0.0;
+                jh[k] = __double2half(w);
+                jl[k] = __double2half(w - static_cast<double>(__half2float(jh[k])));
+                if (__half2float(jl[k]) != 0.0f) p->jlo = true;
+            }
+            if (int rc = upload(&p->dJhi, jh.data(), jh.size())) return rc;
+            if (int rc = upload(&p->dJlo, jl.data(), jl.size())) return rc;
+            const int tb = relax_dense_umma_block();
+            if (!make_tmap_f16_sw128(&p->tm_jhi, p->dJhi, p->np, p->np, 64, tb) ||
+                !make_tmap_f16_sw128(&p->tm_jlo, p->dJlo, p->np, p->np, 64, tb))
+                return fail(MARS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the coupling planes");
+        }
     } else {
         p->np = n;
         if (p->dense) {  // CSR view of a dense store, ascending columns (row_dot order minus zeros)
@@ -305,7 +335,7 @@ struct mars_batch {
     void* d_s0 = nullptr;
     double* d_temp = nullptr;
     int* d_order = nullptr;
-    float* d_work = nullptr;
+    void* d_work = nullptr;
     std::size_t work_bytes = 0;
     int* d_queue = nullptr;
     std::uint8_t* d_status = nullptr;
@@ -319,6 +349,7 @@ struct mars_batch {
     long long* d_best = nullptr;
     int best_grid = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    UmmaLaunch umma{};
 
     ~mars_batch() {
         if (!p) return;
@@ -403,6 +434,9 @@ int batch_alloc(mars_batch* b) {
     if (p->kernel == MARS_KERNEL_DENSE_SIMT) {
         tm = relax_dense_simt_slots_per_cta();
         per_cta = relax_dense_simt_work_bytes(p->np);
+    } else if (p->kernel == MARS_KERNEL_DENSE_UMMA) {
+        tm = relax_dense_umma_slots_per_cta();
+        per_cta = static_cast<std::size_t>(2) * tm * p->np * sizeof(__half);   // S_hi + S_lo rows
     } else {
         tm = relax_csr_slots_per_cta();
         per_cta = relax_csr_work_bytes(p->np);
@@ -412,6 +446,17 @@ int batch_alloc(mars_batch* b) {
     b->slots = b->grid * tm;
     b->work_bytes = per_cta * b->grid;
     CUDA_TRY(cudaMalloc(&b->d_work, b->work_bytes));
+    if (p->kernel == MARS_KERNEL_DENSE_UMMA) {
+        const std::size_t rows = relax_dense_umma_plane_rows(b->grid);
+        b->umma.s_hi = static_cast<__half*>(b->d_work);
+        b->umma.s_lo = b->umma.s_hi + rows * p->np;
+        b->umma.tm_jhi = p->tm_jhi;
+        b->umma.tm_jlo = p->tm_jlo;
+        b->umma.jlo = p->jlo;
+        if (!make_tmap_f16_sw128(&b->umma.tm_shi, b->umma.s_hi, rows, p->np, 64, tm) ||
+            !make_tmap_f16_sw128(&b->umma.tm_slo, b->umma.s_lo, rows, p->np, 64, tm))
+            return fail(MARS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the state planes");
+    }
     return MARS_OK;
 }
 
@@ -681,6 +726,8 @@ int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
     if (b->queue_len > 0) {
         if (p->kernel == MARS_KERNEL_DENSE_SIMT)
             CUDA_TRY(launch_relax_dense_simt(ra, b->grid, st));
+        else if (p->kernel == MARS_KERNEL_DENSE_UMMA)
+            CUDA_TRY(launch_relax_dense_umma(ra, b->umma, b->grid, st));
         else
             CUDA_TRY(launch_relax_csr(ra, b->grid, st));
         ++launches;

@@ -38,6 +38,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <utility>
+
 #include "kernels.cuh"
 #include "slot.cuh"
 #include "umma.cuh"
@@ -72,10 +74,21 @@ struct __align__(8) Ctl {
     volatile std::uint32_t poison_it;
 };
 
-// dynamic smem: [stages: A_hi A_lo J_hi J_lo] [Jd fp32 TB*TB] [Ctl]
+// dynamic smem: [stages: A_hi A_lo J_hi J_lo] [Jtri: upper triangle of the diagonal block,
+// fp32, row i stored from column (i+1) rounded down to a multiple of 4 so every row is
+// float4-aligned] [Sblk: the block's state, fp32 [TB][TM], one column per slot] [Ctl]
+__host__ __device__ constexpr int tri_k0(int i) { return (i + 1) & ~3; }
+__host__ __device__ constexpr int tri_row_off(int i) {
+    int off = 0;
+    for (int r = 0; r < i; ++r) off += TB - tri_k0(r);
+    return off;
+}
 constexpr std::uint32_t SMEM_STAGES = STAGES * STAGE_BYTES;
-constexpr std::uint32_t SMEM_JD = TB * TB * 4;
-constexpr std::uint32_t SMEM_TOTAL = SMEM_STAGES + SMEM_JD + sizeof(Ctl) + 1024;
+constexpr std::uint32_t TRI = tri_row_off(TB);
+constexpr std::uint32_t SMEM_TRI = ((TRI * 4 + 127) / 128) * 128;
+constexpr std::uint32_t SMEM_SBLK = TB * TM * 4;
+constexpr std::uint32_t SMEM_TOTAL = SMEM_STAGES + SMEM_TRI + SMEM_SBLK + sizeof(Ctl);
+static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
 
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
 
@@ -105,6 +118,63 @@ __device__ __forceinline__ void split16(float v, __half& hi, __half& lo, float& 
     back = __half2float(hi) + __half2float(lo);
 }
 
+// runtime tri_row_off: i*TB - sum_{r<i} tri_k0(r), with sum_{m=1..i} floor(m/4) in closed form
+__device__ __forceinline__ int tri_row_off_rt(int i) {
+    const int q = i >> 2, rem = i & 3;
+    return i * TB - 4 * (2 * q * (q - 1) + q * (rem + 1));
+}
+
+// ---- the in-block Gauss-Seidel walk, fully unrolled at compile time (fold expressions):
+// spin I gets its trial value, then every later spin K > I of the block receives
+// J[I][K] * (s_I_new - s_I_old).  phi stays in registers; J rows come from smem as float4.
+struct GsCtx {
+    const float* jtri;
+    float* sblk;          // this slot's column: sblk[i * TM]
+    const float* h;       // field slice or nullptr
+    float Tf;
+    bool quench;
+    int lim;
+    float dmax;
+};
+
+template <int I, int... V>
+__device__ __forceinline__ void gs_update(float (&phi)[TB], const float4* row, float d,
+                                          std::integer_sequence<int, V...>) {
+    // V enumerates float4 groups of row I: columns tri_k0(I) + 4V .. +3
+    ((void)[&] {
+         const float4 j = row[V];
+         constexpr int k = tri_k0(I) + 4 * V;
+         if (k + 0 > I) phi[k + 0] = fmaf(j.x, d, phi[k + 0]);
+         if (k + 1 > I) phi[k + 1] = fmaf(j.y, d, phi[k + 1]);
+         if (k + 2 > I) phi[k + 2] = fmaf(j.z, d, phi[k + 2]);
+         if (k + 3 > I) phi[k + 3] = fmaf(j.w, d, phi[k + 3]);
+     }(),
+     ...);
+}
+
+template <int I>
+__device__ __forceinline__ void gs_step(float (&phi)[TB], GsCtx& c) {
+    if (I < c.lim) {
+        const float x = phi[I] + (c.h ? __ldg(c.h + I) : 0.0f);
+        const float trial = tanh_trial(x, c.Tf, c.quench);
+        __half hh, ll;
+        float snew;
+        split16(trial, hh, ll, snew);
+        const float delta = snew - c.sblk[I * TM];
+        c.sblk[I * TM] = snew;
+        c.dmax = fmaxf(c.dmax, fabsf(delta));
+        if constexpr (I + 1 < TB) {
+            const float4* row = reinterpret_cast<const float4*>(c.jtri + tri_row_off(I));
+            gs_update<I>(phi, row, delta, std::make_integer_sequence<int, (TB - tri_k0(I)) / 4>{});
+        }
+    }
+}
+
+template <int... I>
+__device__ __forceinline__ void gs_block(float (&phi)[TB], GsCtx& c, std::integer_sequence<int, I...>) {
+    (gs_step<I>(phi, c), ...);
+}
+
 template <bool JLO>
 __global__ void __launch_bounds__(NT, 1)
 relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUtensorMap tm_shi,
@@ -112,10 +182,11 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         const __grid_constant__ CUtensorMap tm_jhi,
                         const __grid_constant__ CUtensorMap tm_jlo) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* base = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
-    float* Jd = reinterpret_cast<float*>(base + SMEM_STAGES);
-    Ctl& ctl = *reinterpret_cast<Ctl*>(base + SMEM_STAGES + SMEM_JD);
+    unsigned char* base = smem_raw;   // SWIZZLE_128B tiles need 1024-byte alignment (checked)
+    if (threadIdx.x == 0 && (smem_u32(smem_raw) & 1023u) != 0) __trap();
+    float* Jtri = reinterpret_cast<float*>(base + SMEM_STAGES);
+    float* Sblk = reinterpret_cast<float*>(base + SMEM_STAGES + SMEM_TRI);
+    Ctl& ctl = *reinterpret_cast<Ctl*>(base + SMEM_STAGES + SMEM_TRI + SMEM_SBLK);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int np = a.np, n = a.n, nb = up.nb, nk = np / KC;
@@ -239,15 +310,24 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
             for (int b = 0; b < nb; ++b, ++g) {
                 const int b0 = b * TB;
                 const int lim = min(TB, n - b0);
-                // diagonal block J[b0+i][b0+k] -> smem (after everyone finished the last one)
+                // diagonal block's strict upper triangle -> smem (after the last block's reads)
                 epi_sync();
-                {
-                    const float4* src = reinterpret_cast<const float4*>(a.J32);
-#pragma unroll 4
-                    for (int f = et; f < TB * TB / 4; f += TM) {
-                        const int i = f / (TB / 4), k4 = f % (TB / 4);
-                        reinterpret_cast<float4*>(Jd)[f] =
-                            __ldg(src + (static_cast<size_t>(b0 + i) * np + b0) / 4 + k4);
+                for (int f = et; f < TB * TB / 4; f += TM) {
+                    const int i = f / (TB / 4), k = (f % (TB / 4)) * 4;
+                    if (k >= tri_k0(i))
+                        *reinterpret_cast<float4*>(Jtri + tri_row_off_rt(i) + k - tri_k0(i)) =
+                            __ldg(reinterpret_cast<const float4*>(a.J32 + static_cast<size_t>(b0 + i) * np + b0 + k));
+                }
+                if (active) {   // this slot's block state -> its smem column (overlaps the GEMM)
+#pragma unroll
+                    for (int v = 0; v < TB / 8; ++v) {
+                        const uint4 hv = *reinterpret_cast<const uint4*>(hi_row + b0 + v * 8);
+                        const uint4 lv = *reinterpret_cast<const uint4*>(lo_row + b0 + v * 8);
+                        const __half* h8 = reinterpret_cast<const __half*>(&hv);
+                        const __half* l8 = reinterpret_cast<const __half*>(&lv);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            Sblk[(v * 8 + e) * TM + r] = __half2float(h8[e]) + __half2float(l8[e]);
                     }
                 }
                 epi_sync();
@@ -268,30 +348,22 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
 
                 if (active) {
                     // ---- in-block Gauss-Seidel correction, ascending spin order
-                    __half hbuf[TB], lbuf[TB];
+                    GsCtx ctx{Jtri, Sblk + r, a.h32 ? a.h32 + b0 : nullptr, Tf, quench, lim, 0.0f};
+                    gs_block(phi, ctx, std::make_integer_sequence<int, TB>{});
+                    dmax = fmaxf(dmax, ctx.dmax);
+                    // write back as fp16 pairs (re-splitting hi+lo reproduces the pair)
 #pragma unroll
                     for (int v = 0; v < TB / 8; ++v) {
-                        *reinterpret_cast<uint4*>(&hbuf[v * 8]) = *reinterpret_cast<const uint4*>(hi_row + b0 + v * 8);
-                        *reinterpret_cast<uint4*>(&lbuf[v * 8]) = *reinterpret_cast<const uint4*>(lo_row + b0 + v * 8);
-                    }
+                        uint4 hv, lv;
+                        __half* h8 = reinterpret_cast<__half*>(&hv);
+                        __half* l8 = reinterpret_cast<__half*>(&lv);
 #pragma unroll
-                    for (int i = 0; i < TB; ++i) {
-                        if (i < lim) {
-                            const float x = phi[i] + (a.h32 ? __ldg(a.h32 + b0 + i) : 0.0f);
-                            const float trial = tanh_trial(x, Tf, quench);
-                            float snew;
-                            const float sold = __half2float(hbuf[i]) + __half2float(lbuf[i]);
-                            split16(trial, hbuf[i], lbuf[i], snew);
-                            const float delta = snew - sold;
-                            dmax = fmaxf(dmax, fabsf(delta));
-#pragma unroll
-                            for (int k = i + 1; k < TB; ++k) phi[k] = fmaf(Jd[i * TB + k], delta, phi[k]);
+                        for (int e = 0; e < 8; ++e) {
+                            float back;
+                            split16(Sblk[(v * 8 + e) * TM + r], h8[e], l8[e], back);
                         }
-                    }
-#pragma unroll
-                    for (int v = 0; v < TB / 8; ++v) {
-                        *reinterpret_cast<uint4*>(hi_row + b0 + v * 8) = *reinterpret_cast<const uint4*>(&hbuf[v * 8]);
-                        *reinterpret_cast<uint4*>(lo_row + b0 + v * 8) = *reinterpret_cast<const uint4*>(&lbuf[v * 8]);
+                        *reinterpret_cast<uint4*>(hi_row + b0 + v * 8) = hv;
+                        *reinterpret_cast<uint4*>(lo_row + b0 + v * 8) = lv;
                     }
                 } else if (mode == kLoading || mode == kDrain) {
                     // ---- slot turnover, block by block: old run's spins out, new run's s0 in
@@ -304,12 +376,17 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     }
                     if (mode == kLoading) {
                         const float* src = a.s0 + static_cast<size_t>(new_run) * n + b0;
-                        for (int i = 0; i < TB; ++i) {
-                            __half h, l;
-                            float back;
-                            split16(i < lim ? src[i] : 0.0f, h, l, back);
-                            hi_row[b0 + i] = h;
-                            lo_row[b0 + i] = l;
+                        for (int v = 0; v < TB / 8; ++v) {
+                            uint4 hv, lv;
+                            __half* h8 = reinterpret_cast<__half*>(&hv);
+                            __half* l8 = reinterpret_cast<__half*>(&lv);
+                            for (int e = 0; e < 8; ++e) {
+                                const int i = v * 8 + e;
+                                float back;
+                                split16(i < lim ? src[i] : 0.0f, h8[e], l8[e], back);
+                            }
+                            *reinterpret_cast<uint4*>(hi_row + b0 + v * 8) = hv;
+                            *reinterpret_cast<uint4*>(lo_row + b0 + v * 8) = lv;
                         }
                     }
                 }
@@ -358,6 +435,7 @@ std::size_t relax_dense_umma_plane_rows(int grid) { return static_cast<std::size
 
 cudaError_t launch_relax_dense_umma(const RelaxArgs& a, const UmmaLaunch& u, int grid, cudaStream_t st) {
     UmmaParams up{u.s_hi, u.s_hi, u.s_lo, a.np / TB};
+    if (a.np % TB != 0) return cudaErrorInvalidValue;
     cudaError_t e;
     if (u.jlo) {
         e = cudaFuncSetAttribute(relax_dense_umma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);

@@ -53,9 +53,19 @@ __device__ __forceinline__ bool mbar_try_wait(std::uint64_t* bar, std::uint32_t 
     return ok != 0;
 }
 
-// Wait until the phase with the given parity has completed.
+// Wait until the phase with the given parity has completed.  A pipeline bug must not hang
+// the GPU: after 20 s of waiting the kernel traps (the launch then fails with an error).
 __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
-    while (!mbar_try_wait(bar, parity)) {
+    if (mbar_try_wait(bar, parity)) return;
+    std::uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (std::uint32_t spin = 1;; ++spin) {
+        if (mbar_try_wait(bar, parity)) return;
+        if ((spin & 1023u) == 0) {
+            std::uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 20000000000ull) __trap();
+        }
     }
 }
 
