@@ -42,7 +42,10 @@ struct RelaxArgs {
     long long* iters;
     double* elapsed;
     std::int8_t* spins;        // [count][n] rounded final state (round_spins, model.cpp:245)
+    // optional per-CTA phase counters (clock64 cycles), kProfSlots per CTA, or nullptr
+    long long* prof;
 };
+constexpr int kProfSlots = 16;
 
 // Exact-order energy evaluation (model.cpp:203-229) over `count` rounded spin vectors.
 struct EnergyArgs {

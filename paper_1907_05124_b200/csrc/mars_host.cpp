@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -722,6 +723,13 @@ int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
     ra.elapsed = b->d_elapsed;
     ra.spins = b->d_spins;
     std::int64_t launches = 0;
+    const bool prof = std::getenv("MARS_PROFILE") != nullptr;
+    long long* dprof = nullptr;
+    if (prof) {
+        CUDA_TRY(cudaMalloc(&dprof, sizeof(long long) * kProfSlots * b->grid));
+        CUDA_TRY(cudaMemsetAsync(dprof, 0, sizeof(long long) * kProfSlots * b->grid, st));
+    }
+    ra.prof = dprof;
     CUDA_TRY(cudaEventRecord(b->ev[0], st));
     if (b->queue_len > 0) {
         if (p->kernel == MARS_KERNEL_DENSE_SIMT)
@@ -746,6 +754,22 @@ int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
     CUDA_TRY(cudaEventRecord(b->ev[3], st));
     CUDA_TRY(cudaStreamSynchronize(st));
     b->executed = true;
+    if (prof) {
+        std::vector<long long> h(static_cast<std::size_t>(kProfSlots) * b->grid);
+        CUDA_TRY(cudaMemcpy(h.data(), dprof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+        cudaFree(dprof);
+        double acc[kProfSlots] = {0};
+        for (int c = 0; c < b->grid; ++c)
+            for (int k = 0; k < kProfSlots; ++k) acc[k] += static_cast<double>(h[c * kProfSlots + k]);
+        const double blocks = acc[0] * (h[6] ? h[6] : 1);
+        std::fprintf(stderr,
+                     "[mars prof] grid %d: sweeps/cta %.1f, cycles/cta %.3g | per block: loads %.0f, "
+                     "wait_tmem_full %.0f, correction %.0f, writeback %.0f | producer wait ready %.0f "
+                     "empty %.0f | mma wait full %.0f tmem_empty %.0f\n",
+                     b->grid, acc[0] / b->grid, acc[1] / b->grid, acc[2] / blocks, acc[3] / blocks,
+                     acc[4] / blocks, acc[5] / blocks, acc[8] / blocks, acc[9] / blocks,
+                     acc[10] / blocks, acc[11] / blocks);
+    }
     if (timing) {
         float ms[3];
         CUDA_TRY(cudaEventElapsedTime(&ms[0], b->ev[0], b->ev[1]));

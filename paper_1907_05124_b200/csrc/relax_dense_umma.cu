@@ -126,53 +126,77 @@ __device__ __forceinline__ int tri_row_off_rt(int i) {
 
 // ---- the in-block Gauss-Seidel walk, fully unrolled at compile time (fold expressions):
 // spin I gets its trial value, then every later spin K > I of the block receives
-// J[I][K] * (s_I_new - s_I_old).  phi stays in registers; J rows come from smem as float4.
+// J[I][K] * (s_I_new - s_I_old).  The fields live in registers as packed fp32 pairs so the
+// updates issue as FFMA2 (two FMAs per instruction); J rows come from smem as 16-byte loads.
+using u64 = unsigned long long;
+
+__device__ __forceinline__ float lo32(u64 v) { return __uint_as_float(static_cast<unsigned>(v)); }
+__device__ __forceinline__ float hi32(u64 v) { return __uint_as_float(static_cast<unsigned>(v >> 32)); }
+__device__ __forceinline__ u64 pack2(float a, float b) {
+    return static_cast<u64>(__float_as_uint(a)) | (static_cast<u64>(__float_as_uint(b)) << 32);
+}
+__device__ __forceinline__ void ffma2(u64& acc, u64 a, u64 b) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
+}
+
 struct GsCtx {
     const float* jtri;
     float* sblk;          // this slot's column: sblk[i * TM]
     const float* h;       // field slice or nullptr
-    float Tf;
+    float invT;
     bool quench;
     int lim;
     float dmax;
 };
 
 template <int I, int... V>
-__device__ __forceinline__ void gs_update(float (&phi)[TB], const float4* row, float d,
+__device__ __forceinline__ void gs_update(u64 (&phi)[TB / 2], const ulonglong2* row, float d,
                                           std::integer_sequence<int, V...>) {
-    // V enumerates float4 groups of row I: columns tri_k0(I) + 4V .. +3
+    const u64 dd = pack2(d, d);
+    // V enumerates 16-byte groups of row I: columns k = tri_k0(I) + 4V .. +3
     ((void)[&] {
-         const float4 j = row[V];
+         const ulonglong2 j = row[V];
          constexpr int k = tri_k0(I) + 4 * V;
-         if (k + 0 > I) phi[k + 0] = fmaf(j.x, d, phi[k + 0]);
-         if (k + 1 > I) phi[k + 1] = fmaf(j.y, d, phi[k + 1]);
-         if (k + 2 > I) phi[k + 2] = fmaf(j.z, d, phi[k + 2]);
-         if (k + 3 > I) phi[k + 3] = fmaf(j.w, d, phi[k + 3]);
+         if constexpr (k > I) {
+             ffma2(phi[k / 2], j.x, dd);
+         } else if constexpr (k + 1 > I) {
+             phi[k / 2] = pack2(lo32(phi[k / 2]), fmaf(hi32(j.x), d, hi32(phi[k / 2])));
+         }
+         if constexpr (k + 2 > I) {
+             ffma2(phi[k / 2 + 1], j.y, dd);
+         } else if constexpr (k + 3 > I) {
+             phi[k / 2 + 1] = pack2(lo32(phi[k / 2 + 1]), fmaf(hi32(j.y), d, hi32(phi[k / 2 + 1])));
+         }
      }(),
      ...);
 }
 
 template <int I>
-__device__ __forceinline__ void gs_step(float (&phi)[TB], GsCtx& c) {
+__device__ __forceinline__ void gs_step(u64 (&phi)[TB / 2], GsCtx& c) {
     if (I < c.lim) {
-        const float x = phi[I] + (c.h ? __ldg(c.h + I) : 0.0f);
-        const float trial = tanh_trial(x, c.Tf, c.quench);
-        __half hh, ll;
-        float snew;
-        split16(trial, hh, ll, snew);
-        const float delta = snew - c.sblk[I * TM];
-        c.sblk[I * TM] = snew;
+        const float x = ((I & 1) ? hi32(phi[I / 2]) : lo32(phi[I / 2])) + (c.h ? __ldg(c.h + I) : 0.0f);
+        // tanh_trial (solvers.cpp:145-148): -tanh(phi/t), or -sign(phi) at the quench
+        const float trial = c.quench ? (x > 0.0f ? -1.0f : (x < 0.0f ? 1.0f : 0.0f)) : -tanhf(x * c.invT);
+        const float delta = trial - c.sblk[I * TM];
+        c.sblk[I * TM] = trial;
         c.dmax = fmaxf(c.dmax, fabsf(delta));
         if constexpr (I + 1 < TB) {
-            const float4* row = reinterpret_cast<const float4*>(c.jtri + tri_row_off(I));
+            const ulonglong2* row = reinterpret_cast<const ulonglong2*>(c.jtri + tri_row_off(I));
             gs_update<I>(phi, row, delta, std::make_integer_sequence<int, (TB - tri_k0(I)) / 4>{});
         }
     }
 }
 
 template <int... I>
-__device__ __forceinline__ void gs_block(float (&phi)[TB], GsCtx& c, std::integer_sequence<int, I...>) {
+__device__ __forceinline__ void gs_block(u64 (&phi)[TB / 2], GsCtx& c, std::integer_sequence<int, I...>) {
     (gs_step<I>(phi, c), ...);
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 template <bool JLO>
@@ -221,23 +245,32 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
             tma_prefetch_desc(&tm_jhi);
             if (JLO) tma_prefetch_desc(&tm_jlo);
             std::uint32_t g = 0, it = 0;
+            long long w_ready = 0, w_empty = 0;
             for (;;) {
                 for (int b = 0; b < nb; ++b, ++g) {
                     for (int j = 0; j < nk; ++j, ++it) {
                         if (j == nk - CPB && g > 0) {
                             // the last chunks of GEMM(b) are block b-1: wait for its update
+                            const long long t0 = clock64();
                             mbar_wait(&ctl.chunk_ready, (g - 1) & 1);
+                            w_ready += clock64() - t0;
                             if (ctl.stop) {
                                 const int s = it % STAGES;
                                 mbar_wait(&ctl.empty[s], ((it / STAGES) & 1) ^ 1);
                                 ctl.poison_it = it;
                                 mbar_arrive(&ctl.full[s]);
+                                if (a.prof) {
+                                    a.prof[blockIdx.x * kProfSlots + 8] = w_ready;
+                                    a.prof[blockIdx.x * kProfSlots + 9] = w_empty;
+                                }
                                 goto producer_done;
                             }
                         }
                         const int s = it % STAGES;
                         const int c = (b * CPB + j) % nk;
+                        const long long t1 = clock64();
                         mbar_wait(&ctl.empty[s], ((it / STAGES) & 1) ^ 1);
+                        w_empty += clock64() - t1;
                         unsigned char* st = base + s * STAGE_BYTES;
                         mbar_arrive_expect_tx(&ctl.full[s], JLO ? STAGE_BYTES : STAGE_BYTES - TILE_J);
                         tma_load_2d(st, &tm_shi, &ctl.full[s], c * KC, row0);
@@ -254,16 +287,27 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         if (lane == 0) {
             constexpr std::uint32_t idesc = idesc_f16(TM, TB, 0);
             std::uint32_t g = 0, it = 0;
+            long long w_full = 0, w_tmem = 0;
             for (;;) {
                 for (int b = 0; b < nb; ++b, ++g) {
                     const int buf = g & 1;
+                    const long long t0 = clock64();
                     mbar_wait(&ctl.tmem_empty[buf], ((g >> 1) & 1) ^ 1);
+                    w_tmem += clock64() - t0;
                     tc_fence_after();
                     const std::uint32_t d = tmem + buf * TB;
                     for (int j = 0; j < nk; ++j, ++it) {
                         const int s = it % STAGES;
+                        const long long t1 = clock64();
                         mbar_wait(&ctl.full[s], (it / STAGES) & 1);
-                        if (ctl.poison_it == it) goto mma_done;
+                        w_full += clock64() - t1;
+                        if (ctl.poison_it == it) {
+                            if (a.prof) {
+                                a.prof[blockIdx.x * kProfSlots + 10] = w_full;
+                                a.prof[blockIdx.x * kProfSlots + 11] = w_tmem;
+                            }
+                            goto mma_done;
+                        }
                         tc_fence_after();
                         const std::uint32_t st = smem_u32(base + s * STAGE_BYTES);
 #pragma unroll
@@ -301,22 +345,26 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         int mode = kIdle, old_run = -1, new_run = claim_run(a);
         if (new_run >= 0) mode = kLoading;
         std::uint32_t g = 0;
+        long long c_loads = 0, c_wait = 0, c_corr = 0, c_wb = 0, n_sweeps = 0;
+        const long long c_start = clock64();
 
         for (;;) {
+            ++n_sweeps;
             const bool active = mode == kActive;
             const bool quench = active && slot_quench(slot);
-            const float Tf = static_cast<float>(slot.T);
+            const float invT = 1.0f / static_cast<float>(slot.T);
             float dmax = 0.0f;
             for (int b = 0; b < nb; ++b, ++g) {
                 const int b0 = b * TB;
                 const int lim = min(TB, n - b0);
                 // diagonal block's strict upper triangle -> smem (after the last block's reads)
+                long long t0 = clock64();
                 epi_sync();
-                for (int f = et; f < TB * TB / 4; f += TM) {
+                for (int f = et; f < TB * TB / 4; f += TM) {       // async, all in flight at once
                     const int i = f / (TB / 4), k = (f % (TB / 4)) * 4;
                     if (k >= tri_k0(i))
-                        *reinterpret_cast<float4*>(Jtri + tri_row_off_rt(i) + k - tri_k0(i)) =
-                            __ldg(reinterpret_cast<const float4*>(a.J32 + static_cast<size_t>(b0 + i) * np + b0 + k));
+                        cp_async16(Jtri + tri_row_off_rt(i) + k - tri_k0(i),
+                                   a.J32 + static_cast<size_t>(b0 + i) * np + b0 + k);
                 }
                 if (active) {   // this slot's block state -> its smem column (overlaps the GEMM)
 #pragma unroll
@@ -330,17 +378,22 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                             Sblk[(v * 8 + e) * TM + r] = __half2float(h8[e]) + __half2float(l8[e]);
                     }
                 }
+                cp_async_wait_all();
                 epi_sync();
+                long long t1 = clock64();
+                c_loads += t1 - t0;
                 const int buf = g & 1;
                 mbar_wait(&ctl.tmem_full[buf], (g >> 1) & 1);
+                long long t2 = clock64();
+                c_wait += t2 - t1;
                 tc_fence_after();
-                float phi[TB];
+                u64 phi[TB / 2];
 #pragma unroll
                 for (int c = 0; c < TB / 32; ++c) {
                     float v[32];
                     tmem_ld32(tmem + (static_cast<std::uint32_t>(q * 32) << 16) + buf * TB + c * 32, v);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) phi[c * 32 + j] = v[j];
+                    for (int j = 0; j < 16; ++j) phi[c * 16 + j] = pack2(v[2 * j], v[2 * j + 1]);
                 }
                 tmem_ld_wait();
                 tc_fence_before();
@@ -348,9 +401,12 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
 
                 if (active) {
                     // ---- in-block Gauss-Seidel correction, ascending spin order
-                    GsCtx ctx{Jtri, Sblk + r, a.h32 ? a.h32 + b0 : nullptr, Tf, quench, lim, 0.0f};
+                    GsCtx ctx{Jtri, Sblk + r, a.h32 ? a.h32 + b0 : nullptr, invT, quench, lim, 0.0f};
                     gs_block(phi, ctx, std::make_integer_sequence<int, TB>{});
                     dmax = fmaxf(dmax, ctx.dmax);
+                    const long long t3 = clock64();
+                    c_corr += t3 - t2;
+                    t2 = t3;
                     // write back as fp16 pairs (re-splitting hi+lo reproduces the pair)
 #pragma unroll
                     for (int v = 0; v < TB / 8; ++v) {
@@ -390,6 +446,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         }
                     }
                 }
+                c_wb += clock64() - t2;
                 if (b == nb - 1) {
                     // ---- end of sweep: annealing state machine (solvers.cpp:178-200)
                     if (active) {
@@ -419,7 +476,17 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 }
             }
         }
-    epilogue_done:;
+    epilogue_done:
+        if (a.prof && et == 0) {
+            long long* pr = a.prof + blockIdx.x * kProfSlots;
+            pr[0] = n_sweeps;
+            pr[1] = clock64() - c_start;
+            pr[2] = c_loads;
+            pr[3] = c_wait;
+            pr[4] = c_corr;
+            pr[5] = c_wb;
+            pr[6] = nb;
+        }
     }
     tc_fence_before();
     __syncthreads();
