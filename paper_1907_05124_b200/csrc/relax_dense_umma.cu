@@ -76,7 +76,7 @@ struct __align__(8) Ctl {
 
 // dynamic smem: [stages: A_hi A_lo J_hi J_lo] [Jtri: upper triangle of the diagonal block,
 // fp32, row i stored from column (i+1) rounded down to a multiple of 4 so every row is
-// float4-aligned] [Sblk: the block's state, fp32 [TB][TM], one column per slot] [Ctl]
+// float4-aligned] [Sdel: the block's Delta history, fp32 [TB][TM], one column per slot] [Ctl]
 __host__ __device__ constexpr int tri_k0(int i) { return (i + 1) & ~3; }
 __host__ __device__ constexpr int tri_row_off(int i) {
     int off = 0;
@@ -124,10 +124,12 @@ __device__ __forceinline__ int tri_row_off_rt(int i) {
     return i * TB - 4 * (2 * q * (q - 1) + q * (rem + 1));
 }
 
-// ---- the in-block Gauss-Seidel walk, fully unrolled at compile time (fold expressions):
-// spin I gets its trial value, then every later spin K > I of the block receives
-// J[I][K] * (s_I_new - s_I_old).  The fields live in registers as packed fp32 pairs so the
-// updates issue as FFMA2 (two FMAs per instruction); J rows come from smem as 16-byte loads.
+// ---- the in-block Gauss-Seidel walk.  Two levels: SB-spin sub-blocks walked with a fully
+// unrolled body (fold expressions), inside a runtime loop over the block; before sub-block
+// s walks, every earlier spin's Delta (kept in this thread's smem column) is applied to its
+// fields.  Fields are packed fp32 pairs so the updates issue as FFMA2; J rows come from smem
+// as 16-byte loads.  The compact loop keeps the hot code inside the instruction cache (a
+// fully unrolled 128-spin triangle is ~220 KB of SASS, streamed from L2 by every SM).
 using u64 = unsigned long long;
 
 __device__ __forceinline__ float lo32(u64 v) { return __uint_as_float(static_cast<unsigned>(v)); }
@@ -139,9 +141,11 @@ __device__ __forceinline__ void ffma2(u64& acc, u64 a, u64 b) {
     asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
 }
 
-struct GsCtx {
+constexpr int SB = 16;
+
+struct SubCtx {
     const float* jtri;
-    float* sblk;          // this slot's column: sblk[i * TM]
+    float* sdel;          // this slot's Delta column: sdel[i * TM]
     const float* h;       // field slice or nullptr
     float invT;
     bool quench;
@@ -149,47 +153,97 @@ struct GsCtx {
     float dmax;
 };
 
-template <int I, int... V>
-__device__ __forceinline__ void gs_update(u64 (&phi)[TB / 2], const ulonglong2* row, float d,
-                                          std::integer_sequence<int, V...>) {
+template <int I, int G>
+__device__ __forceinline__ void sub_update_group(u64 (&p)[SB / 2], const float* row, int k0, u64 dd, float d) {
+    // columns k0 + 4G .. +3 of spin row (k0 + I); only columns > I are updated
+    constexpr int m = 4 * G;
+    const ulonglong2 j = *reinterpret_cast<const ulonglong2*>(row + k0 + m);
+    if constexpr (m > I) {
+        ffma2(p[m / 2], j.x, dd);
+    } else if constexpr (m + 1 > I) {
+        p[m / 2] = pack2(lo32(p[m / 2]), fmaf(hi32(j.x), d, hi32(p[m / 2])));
+    }
+    if constexpr (m + 2 > I) {
+        ffma2(p[m / 2 + 1], j.y, dd);
+    } else if constexpr (m + 3 > I) {
+        p[m / 2 + 1] = pack2(lo32(p[m / 2 + 1]), fmaf(hi32(j.y), d, hi32(p[m / 2 + 1])));
+    }
+}
+
+template <int I, int... G>
+__device__ __forceinline__ void sub_update(u64 (&p)[SB / 2], const float* row, int k0, float d,
+                                           std::integer_sequence<int, G...>) {
     const u64 dd = pack2(d, d);
-    // V enumerates 16-byte groups of row I: columns k = tri_k0(I) + 4V .. +3
-    ((void)[&] {
-         const ulonglong2 j = row[V];
-         constexpr int k = tri_k0(I) + 4 * V;
-         if constexpr (k > I) {
-             ffma2(phi[k / 2], j.x, dd);
-         } else if constexpr (k + 1 > I) {
-             phi[k / 2] = pack2(lo32(phi[k / 2]), fmaf(hi32(j.x), d, hi32(phi[k / 2])));
-         }
-         if constexpr (k + 2 > I) {
-             ffma2(phi[k / 2 + 1], j.y, dd);
-         } else if constexpr (k + 3 > I) {
-             phi[k / 2 + 1] = pack2(lo32(phi[k / 2 + 1]), fmaf(hi32(j.y), d, hi32(phi[k / 2 + 1])));
-         }
-     }(),
-     ...);
+    (sub_update_group<I, ((I + 1) & ~3) / 4 + G>(p, row, k0, dd, d), ...);
 }
 
 template <int I>
-__device__ __forceinline__ void gs_step(u64 (&phi)[TB / 2], GsCtx& c) {
-    if (I < c.lim) {
-        const float x = ((I & 1) ? hi32(phi[I / 2]) : lo32(phi[I / 2])) + (c.h ? __ldg(c.h + I) : 0.0f);
+__device__ __forceinline__ void sub_step(u64 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB], int k0,
+                                         SubCtx& c) {
+    if (k0 + I < c.lim) {
+        const float x = ((I & 1) ? hi32(p[I / 2]) : lo32(p[I / 2])) + (c.h ? __ldg(c.h + k0 + I) : 0.0f);
         // tanh_trial (solvers.cpp:145-148): -tanh(phi/t), or -sign(phi) at the quench
         const float trial = c.quench ? (x > 0.0f ? -1.0f : (x < 0.0f ? 1.0f : 0.0f)) : -tanhf(x * c.invT);
-        const float delta = trial - c.sblk[I * TM];
-        c.sblk[I * TM] = trial;
+        const float delta = trial - old[I];
+        c.sdel[(k0 + I) * TM] = delta;
+        nv[I] = trial;
         c.dmax = fmaxf(c.dmax, fabsf(delta));
-        if constexpr (I + 1 < TB) {
-            const ulonglong2* row = reinterpret_cast<const ulonglong2*>(c.jtri + tri_row_off(I));
-            gs_update<I>(phi, row, delta, std::make_integer_sequence<int, (TB - tri_k0(I)) / 4>{});
+        if constexpr (I + 1 < SB) {
+            const int i = k0 + I;
+            const float* row = c.jtri + tri_row_off_rt(i) - tri_k0(i);   // row[k] = J[i][k], k >= tri_k0(i)
+            sub_update<I>(p, row, k0, delta, std::make_integer_sequence<int, SB / 4 - ((I + 1) & ~3) / 4>{});
         }
+    } else {
+        nv[I] = old[I];
     }
 }
 
 template <int... I>
-__device__ __forceinline__ void gs_block(u64 (&phi)[TB / 2], GsCtx& c, std::integer_sequence<int, I...>) {
-    (gs_step<I>(phi, c), ...);
+__device__ __forceinline__ void sub_walk(u64 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB], int k0,
+                                         SubCtx& c, std::integer_sequence<int, I...>) {
+    (sub_step<I>(p, old, nv, k0, c), ...);
+}
+
+__device__ __forceinline__ void tmem_ld16(std::uint32_t taddr, float (&v)[16]) {
+    std::uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void load_old16(const __half* hi, const __half* lo, float (&old)[SB]) {
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+        const uint4 hv = *reinterpret_cast<const uint4*>(hi + v * 8);
+        const uint4 lv = *reinterpret_cast<const uint4*>(lo + v * 8);
+        const __half* h8 = reinterpret_cast<const __half*>(&hv);
+        const __half* l8 = reinterpret_cast<const __half*>(&lv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) old[v * 8 + e] = __half2float(h8[e]) + __half2float(l8[e]);
+    }
+}
+
+__device__ __forceinline__ void store_new16(__half* hi, __half* lo, const float (&nv)[SB]) {
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+        uint4 hv, lv;
+        __half* h8 = reinterpret_cast<__half*>(&hv);
+        __half* l8 = reinterpret_cast<__half*>(&lv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            float back;
+            split16(nv[v * 8 + e], h8[e], l8[e], back);
+        }
+        *reinterpret_cast<uint4*>(hi + v * 8) = hv;
+        *reinterpret_cast<uint4*>(lo + v * 8) = lv;
+    }
 }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -209,7 +263,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
     unsigned char* base = smem_raw;   // SWIZZLE_128B tiles need 1024-byte alignment (checked)
     if (threadIdx.x == 0 && (smem_u32(smem_raw) & 1023u) != 0) __trap();
     float* Jtri = reinterpret_cast<float*>(base + SMEM_STAGES);
-    float* Sblk = reinterpret_cast<float*>(base + SMEM_STAGES + SMEM_TRI);
+    float* Sdel = reinterpret_cast<float*>(base + SMEM_STAGES + SMEM_TRI);
     Ctl& ctl = *reinterpret_cast<Ctl*>(base + SMEM_STAGES + SMEM_TRI + SMEM_SBLK);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -366,18 +420,6 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         cp_async16(Jtri + tri_row_off_rt(i) + k - tri_k0(i),
                                    a.J32 + static_cast<size_t>(b0 + i) * np + b0 + k);
                 }
-                if (active) {   // this slot's block state -> its smem column (overlaps the GEMM)
-#pragma unroll
-                    for (int v = 0; v < TB / 8; ++v) {
-                        const uint4 hv = *reinterpret_cast<const uint4*>(hi_row + b0 + v * 8);
-                        const uint4 lv = *reinterpret_cast<const uint4*>(lo_row + b0 + v * 8);
-                        const __half* h8 = reinterpret_cast<const __half*>(&hv);
-                        const __half* l8 = reinterpret_cast<const __half*>(&lv);
-#pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            Sblk[(v * 8 + e) * TM + r] = __half2float(h8[e]) + __half2float(l8[e]);
-                    }
-                }
                 cp_async_wait_all();
                 epi_sync();
                 long long t1 = clock64();
@@ -387,41 +429,54 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 long long t2 = clock64();
                 c_wait += t2 - t1;
                 tc_fence_after();
-                u64 phi[TB / 2];
-#pragma unroll
-                for (int c = 0; c < TB / 32; ++c) {
-                    float v[32];
-                    tmem_ld32(tmem + (static_cast<std::uint32_t>(q * 32) << 16) + buf * TB + c * 32, v);
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) phi[c * 16 + j] = pack2(v[2 * j], v[2 * j + 1]);
-                }
-                tmem_ld_wait();
-                tc_fence_before();
-                mbar_arrive(&ctl.tmem_empty[buf]);
+                const std::uint32_t tacc = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + buf * TB;
 
-                if (active) {
-                    // ---- in-block Gauss-Seidel correction, ascending spin order
-                    GsCtx ctx{Jtri, Sblk + r, a.h32 ? a.h32 + b0 : nullptr, invT, quench, lim, 0.0f};
-                    gs_block(phi, ctx, std::make_integer_sequence<int, TB>{});
+                if (__any_sync(0xffffffffu, active)) {
+                    // ---- in-block Gauss-Seidel correction, ascending spin order.  Warp-uniform
+                    // (tcgen05.ld is .sync.aligned); lanes of inactive slots compute but never store.
+                    SubCtx ctx{Jtri, Sdel + r, a.h32 ? a.h32 + b0 : nullptr, invT, quench, lim, 0.0f};
+                    float old[SB], nxt[SB];
+                    load_old16(hi_row + b0, lo_row + b0, nxt);
+                    for (int k0 = 0; k0 < TB && k0 < lim; k0 += SB) {
+#pragma unroll
+                        for (int i = 0; i < SB; ++i) old[i] = nxt[i];
+                        if (k0 + SB < TB && k0 + SB < lim)
+                            load_old16(hi_row + b0 + k0 + SB, lo_row + b0 + k0 + SB, nxt);
+                        float pv[SB];
+                        tmem_ld16(tacc + k0, pv);
+                        u64 pf[SB / 2];
+#pragma unroll
+                        for (int j = 0; j < SB / 2; ++j) pf[j] = pack2(pv[2 * j], pv[2 * j + 1]);
+                        // corrections from the block's earlier spins: J[j][k0..k0+SB) * Delta_j
+                        const float* dcol = Sdel + r;
+#pragma unroll 2
+                        for (int j = 0; j < k0; ++j) {
+                            const float d = dcol[j * TM];
+                            const u64 dd = pack2(d, d);
+                            const ulonglong2* jr = reinterpret_cast<const ulonglong2*>(
+                                Jtri + tri_row_off_rt(j) + k0 - tri_k0(j));
+#pragma unroll
+                            for (int m = 0; m < SB / 4; ++m) {
+                                const ulonglong2 jv = jr[m];
+                                ffma2(pf[2 * m], jv.x, dd);
+                                ffma2(pf[2 * m + 1], jv.y, dd);
+                            }
+                        }
+                        float nv[SB];
+                        sub_walk(pf, old, nv, k0, ctx, std::make_integer_sequence<int, SB>{});
+                        if (active) store_new16(hi_row + b0 + k0, lo_row + b0 + k0, nv);
+                    }
                     dmax = fmaxf(dmax, ctx.dmax);
+                    tc_fence_before();
+                    mbar_arrive(&ctl.tmem_empty[buf]);
                     const long long t3 = clock64();
                     c_corr += t3 - t2;
                     t2 = t3;
-                    // write back as fp16 pairs (re-splitting hi+lo reproduces the pair)
-#pragma unroll
-                    for (int v = 0; v < TB / 8; ++v) {
-                        uint4 hv, lv;
-                        __half* h8 = reinterpret_cast<__half*>(&hv);
-                        __half* l8 = reinterpret_cast<__half*>(&lv);
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            float back;
-                            split16(Sblk[(v * 8 + e) * TM + r], h8[e], l8[e], back);
-                        }
-                        *reinterpret_cast<uint4*>(hi_row + b0 + v * 8) = hv;
-                        *reinterpret_cast<uint4*>(lo_row + b0 + v * 8) = lv;
-                    }
-                } else if (mode == kLoading || mode == kDrain) {
+                } else {
+                    tc_fence_before();
+                    mbar_arrive(&ctl.tmem_empty[buf]);
+                }
+                if (!active && (mode == kLoading || mode == kDrain)) {
                     // ---- slot turnover, block by block: old run's spins out, new run's s0 in
                     if (old_run >= 0) {
                         std::int8_t* out = a.spins + static_cast<size_t>(old_run) * n + b0;
