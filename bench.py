@@ -38,6 +38,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-runs", type=int, default=0, help="CPU baseline sample size")
+    ap.add_argument("--n", type=int, default=0, help="profiling: override the instance size")
+    ap.add_argument("--tmax", type=float, default=0.0, help="profiling: override t_max")
     return ap.parse_args()
 
 
@@ -282,6 +284,9 @@ def main():
     args = parse()
     from paper_1907_05124_b200.workloads import WORKLOADS
     w = WORKLOADS[args.workload]
+    if args.n or args.tmax:
+        import dataclasses
+        w = dataclasses.replace(w, name=w.name + "_custom", n=args.n or w.n, t_max=args.tmax or w.t_max)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))

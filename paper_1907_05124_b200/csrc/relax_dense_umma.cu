@@ -28,8 +28,8 @@
 // epilogue streams the old run's final spins out and the new run's initial state in, block
 // by block, in Gauss-Seidel order, so every GEMM always reads a consistent state.
 //
-// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer,
-// warps 2..5 = epilogue (warp w accesses TMEM lanes 32*(w%4) .. +31).
+// Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer,
+// warps 2..9 = epilogue, two per TMEM lane quarter (warp w accesses lanes 32*(w%4) .. +31).
 //
 // Global layout: state planes S_hi/S_lo [grid*TM][np] fp16 (row per slot, K-major for
 // UMMA), couplings J_hi/J_lo [np][np] fp16 (J symmetric, so row i of J is column i: the
@@ -54,8 +54,9 @@ constexpr int TB = 128;      // spins per Gauss-Seidel block = UMMA N
 constexpr int KC = 64;       // K per pipeline stage (one 128-byte swizzle atom of fp16)
 constexpr int CPB = TB / KC; // chunks per block
 constexpr int STAGES = 2;
-constexpr int NT = 192;
+constexpr int NT = 320;             // 2 control warps + 8 epilogue warps
 constexpr int EPI0 = 2;      // first epilogue warp
+constexpr int NEPI = 256;    // epilogue threads
 constexpr std::uint32_t TILE_A = TM * KC * 2;   // 16 KB
 constexpr std::uint32_t TILE_J = TB * KC * 2;   // 16 KB
 constexpr std::uint32_t STAGE_BYTES = 2 * TILE_A + 2 * TILE_J;
@@ -90,14 +91,14 @@ constexpr std::uint32_t SMEM_SBLK = TB * TM * 4;
 constexpr std::uint32_t SMEM_TOTAL = SMEM_STAGES + SMEM_TRI + SMEM_SBLK + sizeof(Ctl);
 static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
 
-__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
 
 __device__ __forceinline__ bool epi_any(bool v) {
     std::uint32_t r;
     asm volatile(
         "{\n\t.reg .pred p, q;\n\t"
         "setp.ne.u32 p, %1, 0;\n\t"
-        "barrier.cta.red.or.pred q, 1, 128, p;\n\t"
+        "barrier.cta.red.or.pred q, 1, 256, p;\n\t"
         "selp.u32 %0, 1, 0, q;\n\t}\n"
         : "=r"(r)
         : "r"(static_cast<std::uint32_t>(v))
@@ -277,9 +278,9 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&ctl.tmem_full[s], 1);
-            mbar_init(&ctl.tmem_empty[s], TM);
+            mbar_init(&ctl.tmem_empty[s], NEPI);
         }
-        mbar_init(&ctl.chunk_ready, TM);
+        mbar_init(&ctl.chunk_ready, NEPI);
         mbar_init(&ctl.mma_done, 1);
         ctl.stop = 0;
         ctl.poison_it = 0xFFFFFFFFu;
@@ -388,16 +389,44 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         __syncwarp();
     } else {
         // ================================================================ epilogue
-        const int q = warp & 3;                 // TMEM lane quarter
-        const int r = q * 32 + lane;            // slot = TMEM lane
-        const int et = threadIdx.x - EPI0 * 32; // 0..127 for cooperative loads
+        // Eight warps, two per TMEM lane quarter: warp pair (w, w+4) owns slots
+        // r = 32*(w%4) + lane and alternates the SB-spin sub-blocks of every block, so one warp
+        // pre-applies the Delta history to its next sub-block while its partner walks the
+        // current one; a pair-private named barrier hands each finished sub-block's Delta over.
+        // Side 0 owns the slot state machine and publishes it to side 1 at sweep ends.
+        const int q = warp & 3;                            // TMEM lane quarter
+        const int side = warp >= EPI0 + 4 ? 1 : 0;
+        const int r = q * 32 + lane;                       // slot = TMEM lane
+        const int et = threadIdx.x - EPI0 * 32;            // 0..255 for cooperative loads
+        // hand-off of sub-block h uses named barrier 2 + 2q + (h & 1): two IDs per pair, so a
+        // producer running ahead can never complete the phase its partner has not reached
+        const int pair_bar = 2 + 2 * q;
         __half* hi_row = up.s_hi_w + static_cast<size_t>(row0 + r) * np;
         __half* lo_row = up.s_lo_w + static_cast<size_t>(row0 + r) * np;
+        // sweep-boundary exchange area (the Delta history is dead between blocks)
+        int* x_mode = reinterpret_cast<int*>(Sdel);
+        int* x_new = x_mode + TM;
+        int* x_old = x_mode + 2 * TM;
+        float* x_invT = reinterpret_cast<float*>(x_mode + 3 * TM);
+        int* x_quench = x_mode + 4 * TM;
+        float* x_dmax = reinterpret_cast<float*>(x_mode + 5 * TM);
 
         Slot slot;
         slot.run = -1;
-        int mode = kIdle, old_run = -1, new_run = claim_run(a);
-        if (new_run >= 0) mode = kLoading;
+        int mode = kIdle, old_run = -1, new_run = -1;
+        float invT = 1.0f;
+        bool quench = false;
+        if (side == 0) {
+            new_run = claim_run(a);
+            mode = new_run >= 0 ? kLoading : kIdle;
+            x_mode[r] = mode;
+            x_new[r] = new_run;
+        }
+        epi_sync();
+        if (side == 1) {
+            mode = x_mode[r];
+            new_run = x_new[r];
+        }
         std::uint32_t g = 0;
         long long c_loads = 0, c_wait = 0, c_corr = 0, c_wb = 0, n_sweeps = 0;
         const long long c_start = clock64();
@@ -405,89 +434,96 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         for (;;) {
             ++n_sweeps;
             const bool active = mode == kActive;
-            const bool quench = active && slot_quench(slot);
-            const float invT = 1.0f / static_cast<float>(slot.T);
             float dmax = 0.0f;
             for (int b = 0; b < nb; ++b, ++g) {
                 const int b0 = b * TB;
                 const int lim = min(TB, n - b0);
-                // diagonal block's strict upper triangle -> smem (after the last block's reads)
+                const int nsub = (lim + SB - 1) / SB;
                 long long t0 = clock64();
+                // diagonal block's upper triangle -> smem, overlapping the wait for GEMM(b)
                 epi_sync();
-                for (int f = et; f < TB * TB / 4; f += TM) {       // async, all in flight at once
+                for (int f = et; f < TB * TB / 4; f += 2 * TM) {
                     const int i = f / (TB / 4), k = (f % (TB / 4)) * 4;
                     if (k >= tri_k0(i))
                         cp_async16(Jtri + tri_row_off_rt(i) + k - tri_k0(i),
                                    a.J32 + static_cast<size_t>(b0 + i) * np + b0 + k);
                 }
-                cp_async_wait_all();
-                epi_sync();
-                long long t1 = clock64();
-                c_loads += t1 - t0;
                 const int buf = g & 1;
+                long long t1 = clock64();
                 mbar_wait(&ctl.tmem_full[buf], (g >> 1) & 1);
                 long long t2 = clock64();
                 c_wait += t2 - t1;
+                cp_async_wait_all();
+                epi_sync();
+                const long long t2b = clock64();
+                c_loads += (t1 - t0) + (t2b - t2);
+                t2 = t2b;
                 tc_fence_after();
                 const std::uint32_t tacc = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + buf * TB;
 
                 if (__any_sync(0xffffffffu, active)) {
-                    // ---- in-block Gauss-Seidel correction, ascending spin order.  Warp-uniform
-                    // (tcgen05.ld is .sync.aligned); lanes of inactive slots compute but never store.
+                    // ---- in-block Gauss-Seidel correction, ascending spin order (warp-uniform:
+                    // tcgen05.ld is .sync.aligned; lanes of inactive slots compute, never store)
                     SubCtx ctx{Jtri, Sdel + r, a.h32 ? a.h32 + b0 : nullptr, invT, quench, lim, 0.0f};
-                    float old[SB], nxt[SB];
-                    load_old16(hi_row + b0, lo_row + b0, nxt);
-                    for (int k0 = 0; k0 < TB && k0 < lim; k0 += SB) {
-#pragma unroll
-                        for (int i = 0; i < SB; ++i) old[i] = nxt[i];
-                        if (k0 + SB < TB && k0 + SB < lim)
-                            load_old16(hi_row + b0 + k0 + SB, lo_row + b0 + k0 + SB, nxt);
+                    const float* dcol = Sdel + r;
+                    for (int s = side; s < nsub; s += 2) {
+                        const int k0 = s * SB;
+                        float old[SB];
+                        load_old16(hi_row + b0 + k0, lo_row + b0 + k0, old);
                         float pv[SB];
                         tmem_ld16(tacc + k0, pv);
                         u64 pf[SB / 2];
 #pragma unroll
                         for (int j = 0; j < SB / 2; ++j) pf[j] = pack2(pv[2 * j], pv[2 * j + 1]);
-                        // corrections from the block's earlier spins: J[j][k0..k0+SB) * Delta_j
-                        const float* dcol = Sdel + r;
+                        // corrections J[j][k0..k0+SB) * Delta_j: first every Delta already final
+                        // (sub-blocks < s-1), then -- after the partner hands it over -- s-1's
+                        const int jpre = s > 0 ? k0 - SB : 0;
+                        for (int pass = 0; pass < 2; ++pass) {
+                            const int jb = pass == 0 ? 0 : jpre, je = pass == 0 ? jpre : k0;
+                            if (pass == 1) {
+                                if (s == 0) break;
+                                asm volatile("bar.sync %0, 64;\n" ::"r"(pair_bar + ((s - 1) & 1)) : "memory");
+                            }
 #pragma unroll 2
-                        for (int j = 0; j < k0; ++j) {
-                            const float d = dcol[j * TM];
-                            const u64 dd = pack2(d, d);
-                            const ulonglong2* jr = reinterpret_cast<const ulonglong2*>(
-                                Jtri + tri_row_off_rt(j) + k0 - tri_k0(j));
+                            for (int j = jb; j < je; ++j) {
+                                const float d = dcol[j * TM];
+                                const u64 dd = pack2(d, d);
+                                const ulonglong2* jr = reinterpret_cast<const ulonglong2*>(
+                                    Jtri + tri_row_off_rt(j) + k0 - tri_k0(j));
 #pragma unroll
-                            for (int m = 0; m < SB / 4; ++m) {
-                                const ulonglong2 jv = jr[m];
-                                ffma2(pf[2 * m], jv.x, dd);
-                                ffma2(pf[2 * m + 1], jv.y, dd);
+                                for (int m = 0; m < SB / 4; ++m) {
+                                    const ulonglong2 jv = jr[m];
+                                    ffma2(pf[2 * m], jv.x, dd);
+                                    ffma2(pf[2 * m + 1], jv.y, dd);
+                                }
                             }
                         }
                         float nv[SB];
                         sub_walk(pf, old, nv, k0, ctx, std::make_integer_sequence<int, SB>{});
                         if (active) store_new16(hi_row + b0 + k0, lo_row + b0 + k0, nv);
+                        if (s + 1 < nsub) asm volatile("bar.arrive %0, 64;\n" ::"r"(pair_bar + (s & 1)) : "memory");
                     }
                     dmax = fmaxf(dmax, ctx.dmax);
-                    tc_fence_before();
-                    mbar_arrive(&ctl.tmem_empty[buf]);
-                    const long long t3 = clock64();
-                    c_corr += t3 - t2;
-                    t2 = t3;
-                } else {
-                    tc_fence_before();
-                    mbar_arrive(&ctl.tmem_empty[buf]);
                 }
+                tc_fence_before();
+                mbar_arrive(&ctl.tmem_empty[buf]);
+                const long long t3 = clock64();
+                c_corr += t3 - t2;
+                t2 = t3;
                 if (!active && (mode == kLoading || mode == kDrain)) {
-                    // ---- slot turnover, block by block: old run's spins out, new run's s0 in
+                    // ---- slot turnover, block by block (each side one half of the columns):
+                    // the old run's rounded spins out, the new run's initial state in
+                    const int c0 = side * (TB / 2), c1 = c0 + TB / 2;
                     if (old_run >= 0) {
                         std::int8_t* out = a.spins + static_cast<size_t>(old_run) * n + b0;
-                        for (int i = 0; i < lim; ++i) {                   // round_spins (model.cpp:245)
+                        for (int i = c0; i < c1 && i < lim; ++i) {        // round_spins (model.cpp:245)
                             const float s = __half2float(hi_row[b0 + i]) + __half2float(lo_row[b0 + i]);
                             out[i] = s < 0.0f ? -1 : 1;
                         }
                     }
                     if (mode == kLoading) {
                         const float* src = a.s0 + static_cast<size_t>(new_run) * n + b0;
-                        for (int v = 0; v < TB / 8; ++v) {
+                        for (int v = c0 / 8; v < c1 / 8; ++v) {
                             uint4 hv, lv;
                             __half* h8 = reinterpret_cast<__half*>(&hv);
                             __half* l8 = reinterpret_cast<__half*>(&lv);
@@ -503,24 +539,44 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 }
                 c_wb += clock64() - t2;
                 if (b == nb - 1) {
-                    // ---- end of sweep: annealing state machine (solvers.cpp:178-200)
-                    if (active) {
-                        const int code = slot_after_sweep(slot, dmax, a);
-                        if (code != kSlotContinue) {
-                            slot_finish(slot, code, a);
-                            old_run = slot.run;
-                            new_run = claim_run(a);
-                            mode = new_run >= 0 ? kLoading : kDrain;
+                    // ---- end of sweep: annealing state machine (solvers.cpp:178-200), side 0
+                    epi_sync();                                   // walks done: Sdel is scratch
+                    if (side == 1) x_dmax[r] = dmax;
+                    epi_sync();
+                    if (side == 0) {
+                        dmax = fmaxf(dmax, x_dmax[r]);
+                        if (active) {
+                            const int code = slot_after_sweep(slot, dmax, a);
+                            if (code != kSlotContinue) {
+                                slot_finish(slot, code, a);
+                                old_run = slot.run;
+                                new_run = claim_run(a);
+                                mode = new_run >= 0 ? kLoading : kDrain;
+                            }
+                        } else if (mode == kLoading) {
+                            slot_start(slot, new_run, a);
+                            mode = kActive;
+                            old_run = -1;
+                        } else if (mode == kDrain) {
+                            mode = kIdle;
+                            old_run = -1;
                         }
-                    } else if (mode == kLoading) {
-                        slot_start(slot, new_run, a);
-                        mode = kActive;
-                        old_run = -1;
-                    } else if (mode == kDrain) {
-                        mode = kIdle;
-                        old_run = -1;
+                        quench = mode == kActive && slot_quench(slot);
+                        invT = 1.0f / static_cast<float>(slot.T);
+                        x_mode[r] = mode;
+                        x_new[r] = new_run;
+                        x_old[r] = old_run;
+                        x_invT[r] = invT;
+                        x_quench[r] = quench;
                     }
-                    const bool more = epi_any(mode != kIdle);
+                    const bool more = epi_any(side == 0 && mode != kIdle);
+                    if (side == 1) {
+                        mode = x_mode[r];
+                        new_run = x_new[r];
+                        old_run = x_old[r];
+                        invT = x_invT[r];
+                        quench = x_quench[r] != 0;
+                    }
                     if (!more && et == 0) ctl.stop = 1;
                     fence_proxy_async_global();
                     mbar_arrive(&ctl.chunk_ready);
