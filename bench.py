@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--cpu-runs", type=int, default=0, help="CPU baseline sample size")
     ap.add_argument("--n", type=int, default=0, help="profiling: override the instance size")
     ap.add_argument("--tmax", type=float, default=0.0, help="profiling: override t_max")
+    ap.add_argument("--no-clocks", action="store_true", help="do not sample nvidia-smi")
     return ap.parse_args()
 
 
@@ -57,6 +58,8 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        if self.index < 0:
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
@@ -189,7 +192,7 @@ def run_b200(args, w, rank, world, local_rank, dist):
         batch.execute()
     barrier()
     timings = []
-    with ClockSampler(local_rank) as clocks:
+    with ClockSampler(-1 if args.no_clocks else local_rank) as clocks:
         t_wall = time.perf_counter()
         for _ in range(args.steps):
             timings.append(batch.execute())

@@ -199,7 +199,7 @@ constexpr double kCsrDensity = 0.10;
 int resolve_kernel(mars_problem* p, int requested) {
     if (requested == MARS_KERNEL_AUTO) {
         const double density = static_cast<double>(p->nnz) / (static_cast<double>(p->n) * p->n);
-        return (!p->dense || density < kCsrDensity) ? MARS_KERNEL_CSR : MARS_KERNEL_DENSE_SIMT;
+        return (!p->dense || density < kCsrDensity) ? MARS_KERNEL_CSR : MARS_KERNEL_DENSE_UMMA;
     }
     if (requested == MARS_KERNEL_DENSE_SIMT || requested == MARS_KERNEL_CSR ||
         requested == MARS_KERNEL_DENSE_UMMA)
@@ -769,6 +769,9 @@ int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
                      b->grid, acc[0] / b->grid, acc[1] / b->grid, acc[2] / blocks, acc[3] / blocks,
                      acc[4] / blocks, acc[5] / blocks, acc[8] / blocks, acc[9] / blocks,
                      acc[10] / blocks, acc[11] / blocks);
+        if (acc[13] > 0)
+            std::fprintf(stderr, "[mars prof] side-0 per walk: walk %.0f, pass0 %.0f, handoff %.0f, pass1 %.0f (%.0f walks/cta)\n",
+                         acc[12] / acc[13], acc[14] / acc[13], acc[15] / acc[13], acc[7] / acc[13], acc[13] / b->grid);
     }
     if (timing) {
         float ms[3];

@@ -128,81 +128,89 @@ __device__ __forceinline__ int tri_row_off_rt(int i) {
 // ---- the in-block Gauss-Seidel walk.  Two levels: SB-spin sub-blocks walked with a fully
 // unrolled body (fold expressions), inside a runtime loop over the block; before sub-block
 // s walks, every earlier spin's Delta (kept in this thread's smem column) is applied to its
-// fields.  Fields are packed fp32 pairs so the updates issue as FFMA2; J rows come from smem
-// as 16-byte loads.  The compact loop keeps the hot code inside the instruction cache (a
-// fully unrolled 128-spin triangle is ~220 KB of SASS, streamed from L2 by every SM).
-using u64 = unsigned long long;
-
-__device__ __forceinline__ float lo32(u64 v) { return __uint_as_float(static_cast<unsigned>(v)); }
-__device__ __forceinline__ float hi32(u64 v) { return __uint_as_float(static_cast<unsigned>(v >> 32)); }
-__device__ __forceinline__ u64 pack2(float a, float b) {
-    return static_cast<u64>(__float_as_uint(a)) | (static_cast<u64>(__float_as_uint(b)) << 32);
-}
-__device__ __forceinline__ void ffma2(u64& acc, u64 a, u64 b) {
-    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
-}
-
+// fields.  Fields are fp32 pairs so the updates issue as FFMA2; J rows come from smem as
+// 16-byte loads issued before the spin's trial so their latency hides under the tanh.  The
+// compact loop keeps the hot code inside the instruction cache (a fully unrolled 128-spin
+// triangle is ~220 KB of SASS, streamed from L2 by every SM).
 constexpr int SB = 16;
 
 struct SubCtx {
     const float* jtri;
     float* sdel;          // this slot's Delta column: sdel[i * TM]
     const float* h;       // field slice or nullptr
-    float invT;
+    float invT;           // 1/T, or 0 at the quench
     bool quench;
     int lim;
     float dmax;
 };
 
+__device__ __forceinline__ float2 ffma2(float2 a, float b, float2 c) {
+    return __ffma2_rn(a, make_float2(b, b), c);
+}
+
 template <int I, int G>
-__device__ __forceinline__ void sub_update_group(u64 (&p)[SB / 2], const float* row, int k0, u64 dd, float d) {
-    // columns k0 + 4G .. +3 of spin row (k0 + I); only columns > I are updated
+__device__ __forceinline__ void sub_update_group(float2 (&p)[SB / 2], const float4 j, float d) {
+    // columns 4G .. 4G+3 of spin row I; only columns > I are updated
     constexpr int m = 4 * G;
-    const ulonglong2 j = *reinterpret_cast<const ulonglong2*>(row + k0 + m);
     if constexpr (m > I) {
-        ffma2(p[m / 2], j.x, dd);
+        p[m / 2] = ffma2(make_float2(j.x, j.y), d, p[m / 2]);
     } else if constexpr (m + 1 > I) {
-        p[m / 2] = pack2(lo32(p[m / 2]), fmaf(hi32(j.x), d, hi32(p[m / 2])));
+        p[m / 2].y = fmaf(j.y, d, p[m / 2].y);
     }
     if constexpr (m + 2 > I) {
-        ffma2(p[m / 2 + 1], j.y, dd);
+        p[m / 2 + 1] = ffma2(make_float2(j.z, j.w), d, p[m / 2 + 1]);
     } else if constexpr (m + 3 > I) {
-        p[m / 2 + 1] = pack2(lo32(p[m / 2 + 1]), fmaf(hi32(j.y), d, hi32(p[m / 2 + 1])));
+        p[m / 2 + 1].y = fmaf(j.w, d, p[m / 2 + 1].y);
     }
 }
 
 template <int I, int... G>
-__device__ __forceinline__ void sub_update(u64 (&p)[SB / 2], const float* row, int k0, float d,
+__device__ __forceinline__ void sub_update(float2 (&p)[SB / 2], const float4 (&jr)[SB / 4], float d,
                                            std::integer_sequence<int, G...>) {
-    const u64 dd = pack2(d, d);
-    (sub_update_group<I, ((I + 1) & ~3) / 4 + G>(p, row, k0, dd, d), ...);
+    (sub_update_group<I, ((I + 1) & ~3) / 4 + G>(p, jr[((I + 1) & ~3) / 4 + G], d), ...);
 }
 
-template <int I>
-__device__ __forceinline__ void sub_step(u64 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB], int k0,
+template <int I, bool FULL, bool HAS_H>
+__device__ __forceinline__ void sub_step(float2 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB], int k0,
                                          SubCtx& c) {
-    if (k0 + I < c.lim) {
-        const float x = ((I & 1) ? hi32(p[I / 2]) : lo32(p[I / 2])) + (c.h ? __ldg(c.h + k0 + I) : 0.0f);
+    if (FULL || k0 + I < c.lim) {
+        // J[k0+I][k0 + 4g ..] for the groups this spin updates, issued before the trial
+        float4 jr[SB / 4];
+        if constexpr (I + 1 < SB) {
+            const int i = k0 + I;
+            const float* row = c.jtri + tri_row_off_rt(i) - tri_k0(i) + k0;   // row[m] = J[i][k0+m]
+#pragma unroll
+            for (int g = ((I + 1) & ~3) / 4; g < SB / 4; ++g) jr[g] = *reinterpret_cast<const float4*>(row + 4 * g);
+        }
+        const float x = (I & 1 ? p[I / 2].y : p[I / 2].x) + (HAS_H ? __ldg(c.h + k0 + I) : 0.0f);
         // tanh_trial (solvers.cpp:145-148): -tanh(phi/t), or -sign(phi) at the quench
-        const float trial = c.quench ? (x > 0.0f ? -1.0f : (x < 0.0f ? 1.0f : 0.0f)) : -tanhf(x * c.invT);
+        const float sgn = x > 0.0f ? -1.0f : (x < 0.0f ? 1.0f : 0.0f);
+        const float th = -tanhf(x * c.invT);
+        const float trial = c.quench ? sgn : th;
         const float delta = trial - old[I];
         c.sdel[(k0 + I) * TM] = delta;
         nv[I] = trial;
         c.dmax = fmaxf(c.dmax, fabsf(delta));
-        if constexpr (I + 1 < SB) {
-            const int i = k0 + I;
-            const float* row = c.jtri + tri_row_off_rt(i) - tri_k0(i);   // row[k] = J[i][k], k >= tri_k0(i)
-            sub_update<I>(p, row, k0, delta, std::make_integer_sequence<int, SB / 4 - ((I + 1) & ~3) / 4>{});
-        }
+        if constexpr (I + 1 < SB)
+            sub_update<I>(p, jr, delta, std::make_integer_sequence<int, SB / 4 - ((I + 1) & ~3) / 4>{});
     } else {
         nv[I] = old[I];
     }
 }
 
-template <int... I>
-__device__ __forceinline__ void sub_walk(u64 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB], int k0,
+template <bool FULL, bool HAS_H, int... I>
+__device__ __forceinline__ void sub_walk(float2 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB], int k0,
                                          SubCtx& c, std::integer_sequence<int, I...>) {
-    (sub_step<I>(p, old, nv, k0, c), ...);
+    (sub_step<I, FULL, HAS_H>(p, old, nv, k0, c), ...);
+}
+
+template <bool HAS_H>
+__device__ __forceinline__ void walk_dispatch(float2 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB],
+                                              int k0, SubCtx& c) {
+    if (k0 + SB <= c.lim)
+        sub_walk<true, HAS_H>(p, old, nv, k0, c, std::make_integer_sequence<int, SB>{});
+    else
+        sub_walk<false, HAS_H>(p, old, nv, k0, c, std::make_integer_sequence<int, SB>{});
 }
 
 __device__ __forceinline__ void tmem_ld16(std::uint32_t taddr, float (&v)[16]) {
@@ -429,6 +437,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         }
         std::uint32_t g = 0;
         long long c_loads = 0, c_wait = 0, c_corr = 0, c_wb = 0, n_sweeps = 0;
+        long long c_walk = 0, c_pass0 = 0, c_hand = 0, c_pass1 = 0, n_walks = 0;
         const long long c_start = clock64();
 
         for (;;) {
@@ -472,34 +481,43 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         load_old16(hi_row + b0 + k0, lo_row + b0 + k0, old);
                         float pv[SB];
                         tmem_ld16(tacc + k0, pv);
-                        u64 pf[SB / 2];
+                        float2 pf[SB / 2];
 #pragma unroll
-                        for (int j = 0; j < SB / 2; ++j) pf[j] = pack2(pv[2 * j], pv[2 * j + 1]);
+                        for (int j = 0; j < SB / 2; ++j) pf[j] = make_float2(pv[2 * j], pv[2 * j + 1]);
                         // corrections J[j][k0..k0+SB) * Delta_j: first every Delta already final
                         // (sub-blocks < s-1), then -- after the partner hands it over -- s-1's
                         const int jpre = s > 0 ? k0 - SB : 0;
+                        long long tp = clock64();
                         for (int pass = 0; pass < 2; ++pass) {
                             const int jb = pass == 0 ? 0 : jpre, je = pass == 0 ? jpre : k0;
                             if (pass == 1) {
                                 if (s == 0) break;
+                                const long long ta = clock64();
+                                c_pass0 += ta - tp;
                                 asm volatile("bar.sync %0, 64;\n" ::"r"(pair_bar + ((s - 1) & 1)) : "memory");
+                                tp = clock64();
+                                c_hand += tp - ta;
                             }
 #pragma unroll 2
                             for (int j = jb; j < je; ++j) {
                                 const float d = dcol[j * TM];
-                                const u64 dd = pack2(d, d);
-                                const ulonglong2* jr = reinterpret_cast<const ulonglong2*>(
+                                const float4* jr = reinterpret_cast<const float4*>(
                                     Jtri + tri_row_off_rt(j) + k0 - tri_k0(j));
 #pragma unroll
                                 for (int m = 0; m < SB / 4; ++m) {
-                                    const ulonglong2 jv = jr[m];
-                                    ffma2(pf[2 * m], jv.x, dd);
-                                    ffma2(pf[2 * m + 1], jv.y, dd);
+                                    const float4 jv = jr[m];
+                                    pf[2 * m] = ffma2(make_float2(jv.x, jv.y), d, pf[2 * m]);
+                                    pf[2 * m + 1] = ffma2(make_float2(jv.z, jv.w), d, pf[2 * m + 1]);
                                 }
                             }
                         }
                         float nv[SB];
-                        sub_walk(pf, old, nv, k0, ctx, std::make_integer_sequence<int, SB>{});
+                        const long long tw = clock64();
+                        if (s > 0) c_pass1 += tw - tp; else c_pass0 += tw - tp;
+                        if (ctx.h) walk_dispatch<true>(pf, old, nv, k0, ctx);
+                        else walk_dispatch<false>(pf, old, nv, k0, ctx);
+                        c_walk += clock64() - tw;
+                        ++n_walks;
                         if (active) store_new16(hi_row + b0 + k0, lo_row + b0 + k0, nv);
                         if (s + 1 < nsub) asm volatile("bar.arrive %0, 64;\n" ::"r"(pair_bar + (s & 1)) : "memory");
                     }
@@ -562,7 +580,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                             old_run = -1;
                         }
                         quench = mode == kActive && slot_quench(slot);
-                        invT = 1.0f / static_cast<float>(slot.T);
+                        invT = quench ? 0.0f : 1.0f / static_cast<float>(slot.T);
                         x_mode[r] = mode;
                         x_new[r] = new_run;
                         x_old[r] = old_run;
@@ -597,6 +615,11 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
             pr[4] = c_corr;
             pr[5] = c_wb;
             pr[6] = nb;
+            pr[12] = c_walk;
+            pr[13] = n_walks;
+            pr[14] = c_pass0 + (c_pass1 << 0) * 0;
+            pr[15] = c_hand;
+            pr[7] = c_pass1;
         }
     }
     tc_fence_before();

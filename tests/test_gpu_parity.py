@@ -55,7 +55,7 @@ def compare_records(stats, g, n, prefix="", frac=SPIN_FRACTION, count=None):
 def test_cfg1_full_batch_matches_reference(port):
     w = WORKLOADS["cfg1_sk256_pm1"]
     g = golden("cfg1")
-    p = build_problem(w)
+    p = build_problem(w, kernel="dense_simt")
     assert p.kernel() == "dense_simt"
     stats = mb.run_batch(p, mb.BatchSpec(w.params(), w.runs, w.base_seed, keep_spins=True))
     compare_records(stats, g, w.n)
