@@ -1,0 +1,74 @@
+// adapter_check.cpp -- TEST ONLY: the reference's own code path next to the drop-in GPU
+// adapter, on the same IsingProblem objects built by the reference library.  Prints one line
+// per case: reference vs GPU best energy, identical-spin fraction, hit counts.
+#include <cmath>
+#include <cstdio>
+
+#include "mars/rng.hpp"
+#include "mars/runner.hpp"
+#include "mars_gpu_adapter.hpp"
+
+// generate_sk's loop (io.cpp:151-163) with the reference's own Rng, without linking io.cpp
+static mars::IsingProblem sk(int n, uint64_t seed) {
+    mars::Rng rng(seed);
+    std::vector<double> j(static_cast<size_t>(n) * n, 0.0);
+    for (int i = 0; i < n; ++i)
+        for (int k = i + 1; k < n; ++k) {
+            const double w = rng.gaussian();
+            j[static_cast<size_t>(i) * n + k] = w;
+            j[static_cast<size_t>(k) * n + i] = w;
+        }
+    return mars::IsingProblem::dense(n, std::move(j));
+}
+
+int main() {
+    using namespace mars;
+    int failures = 0;
+    auto compare = [&](const char* name, const IsingProblem& p, const MarsParams& mp, int64_t runs,
+                       uint64_t seed, double min_same) {
+        BatchSpec spec;
+        spec.params = mp;
+        spec.runs = runs;
+        spec.base_seed = seed;
+        spec.workers = 0;
+        const BatchStats ref = run_batch(p, spec);          // the reference (CPU)
+        const BatchStats gpu = gpu::run_batch(p, spec);     // the drop-in (B200)
+        int same = 0, total = 0;
+        for (size_t k = 0; k < ref.runs.size(); ++k) {
+            if (ref.runs[k].status != RunStatus::Ok) continue;
+            ++total;
+            if (ref.runs[k].spins == gpu.runs[k].spins) {
+                ++same;
+                if (ref.runs[k].energy != gpu.runs[k].energy) ++failures;   // bit-exact energies
+            }
+        }
+        const double frac = total ? static_cast<double>(same) / total : 1.0;
+        const bool ok = frac >= min_same && gpu.runs.size() == ref.runs.size() &&
+                        gpu.skipped_runs == ref.skipped_runs &&
+                        std::abs(gpu.best_energy - ref.best_energy) <= 1e-6 * std::abs(ref.best_energy) + 1e-9;
+        if (!ok) ++failures;
+        std::printf("%-28s ref best %.6f  gpu best %.6f  same spins %d/%d  hits %lld/%lld  %s\n", name,
+                    ref.best_energy, gpu.best_energy, same, total, static_cast<long long>(ref.hit_count),
+                    static_cast<long long>(gpu.hit_count), ok ? "OK" : "FAIL");
+    };
+    MarsParams grid;
+    grid.t_min = 0;
+    grid.t_max = 10;
+    grid.t_step = 0.1;
+    // acceptance.cpp:59-82 shape: SK(14) grid sweeps
+    for (uint64_t i = 1; i <= 3; ++i) compare("sk14 grid (acceptance c1)", sk(14, 900000 + i), grid, 1, i, 0.95);
+    MarsParams uni;
+    uni.t_min = 0;
+    uni.t_max = 16;
+    uni.start_mode = StartMode::UniformRandom;
+    compare("sk60 uniform", sk(60, 99), uni, 256, 41, 0.9);
+    // sparse storage path (CSR kernel)
+    std::vector<IsingProblem::Edge> edges;
+    Rng r(31);
+    for (int a = 0; a < 300; ++a)
+        for (int b = a + 1; b < 300; ++b)
+            if (r.uniform_open01() < 0.02) edges.push_back({a, b, r.uniform_open01() < 0.5 ? -1.0 : 1.0});
+    compare("er300 (CSR)", IsingProblem::from_edges(300, edges), uni, 256, 5, 0.98);
+    std::printf("%s\n", failures ? "ADAPTER FAIL" : "ADAPTER OK");
+    return failures ? 1 : 0;
+}

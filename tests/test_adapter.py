@@ -1,0 +1,39 @@
+"""The drop-in seam from the reference's side: tests/cuda/mars_gpu_adapter.hpp keeps the
+reference's `run_batch(const IsingProblem&, const BatchSpec&)` signature and routes MARS
+batches through the C-ABI.  Built here against the reference's own headers and sources
+(/root/reference/proj; the binary travels to the GPU box), run on the B200."""
+import os
+import subprocess
+
+import pytest
+
+from conftest import ROOT, gpu_available
+
+REF = "/root/reference/proj"
+BIN = os.path.join(ROOT, "tests", "cuda", "adapter_check")
+
+
+def build_adapter_check():
+    lib_dir = os.path.join(ROOT, "paper_1907_05124_b200")
+    cmd = ["g++", "-std=c++20", "-O2", f"-I{REF}/include", f"-I{ROOT}/include",
+           f"-I{ROOT}/tests/cuda", os.path.join(ROOT, "tests", "cuda", "adapter_check.cpp"),
+           f"{REF}/src/model.cpp", f"{REF}/src/solvers.cpp", f"{REF}/src/runner.cpp",
+           f"-L{lib_dir}", "-lmars_b200", f"-Wl,-rpath,{lib_dir}", "-Wl,-rpath,$ORIGIN/../../paper_1907_05124_b200",
+           "-lpthread", "-o", BIN]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+
+
+@pytest.mark.skipif(not os.path.isdir(REF), reason="reference sources not present")
+def test_adapter_compiles_against_reference_headers():
+    build_adapter_check()
+    assert os.path.exists(BIN)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")
+def test_adapter_matches_reference_run_batch():
+    if not os.path.exists(BIN):
+        pytest.skip("adapter_check not built (built where /root/reference exists)")
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0 and "ADAPTER OK" in r.stdout, r.stdout + r.stderr
