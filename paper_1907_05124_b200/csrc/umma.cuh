@@ -181,3 +181,41 @@ __host__ __device__ constexpr std::uint32_t idesc_f16(int M, int N, int ab_forma
 
 }  // namespace umma
 }  // namespace marsb200
+
+namespace marsb200 {
+namespace umma {
+
+// D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16.  A (M=128 rows on lanes, K=16 fp16 per
+// instruction) occupies 8 consecutive 32-bit TMEM columns, two fp16 per column.
+__device__ __forceinline__ void mma_f16_ts(std::uint32_t d_tmem, std::uint32_t a_tmem, std::uint64_t bdesc,
+                                           std::uint32_t idesc, std::uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// 32 lanes x 32 bit x 8 columns store: thread t of the warp writes lane (base + t).
+__device__ __forceinline__ void tmem_st8(std::uint32_t taddr, const std::uint32_t (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr),
+                 "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(std::uint32_t taddr, const std::uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_st_wait() {
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+
+}  // namespace umma
+}  // namespace marsb200
