@@ -217,17 +217,22 @@ __device__ __forceinline__ void sub_update(float2 (&p)[SB / 2], const float4 (&j
     (sub_update_group<I, ((I + 1) & ~3) / 4 + G>(p, jr[((I + 1) & ~3) / 4 + G], d), ...);
 }
 
-template <int I, bool FULL, bool HAS_H>
-__device__ __forceinline__ void sub_step(float2 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB],
-                                         float (&dl)[SB], int k0, SubCtx& c) {
+template <int I, bool FULL, bool HAS_H, bool NEXT>
+__device__ __forceinline__ void sub_step(float2 (&p)[SB / 2], float2 (&cn)[SB / 2], const float (&old)[SB],
+                                         float (&nv)[SB], int k0, SubCtx& c) {
     if (FULL || k0 + I < c.lim) {
-        // J[k0+I][k0 + 4g ..] for the groups this spin updates, issued before the trial
+        const int i = k0 + I;
+        const float* row = c.jtri + tri_row_off_rt(i) - tri_k0(i) + k0;   // row[m] = J[i][k0+m]
+        // J[i][k0 + 4g ..] for the groups this spin updates, issued before the trial
         float4 jr[SB / 4];
         if constexpr (I + 1 < SB) {
-            const int i = k0 + I;
-            const float* row = c.jtri + tri_row_off_rt(i) - tri_k0(i) + k0;   // row[m] = J[i][k0+m]
 #pragma unroll
             for (int g = ((I + 1) & ~3) / 4; g < SB / 4; ++g) jr[g] = *reinterpret_cast<const float4*>(row + 4 * g);
+        }
+        float4 jn[SB / 4];
+        if constexpr (NEXT) {
+#pragma unroll
+            for (int g = 0; g < SB / 4; ++g) jn[g] = *reinterpret_cast<const float4*>(row + SB + 4 * g);
         }
         const float x = (I & 1 ? p[I / 2].y : p[I / 2].x) + (HAS_H ? __ldg(c.h + k0 + I) : 0.0f);
         // tanh_trial (solvers.cpp:145-148): -tanh(phi/t), or -sign(phi) at the quench
@@ -236,29 +241,38 @@ __device__ __forceinline__ void sub_step(float2 (&p)[SB / 2], const float (&old)
         const float trial = c.quench ? sgn : th;
         const float delta = trial - old[I];
         nv[I] = trial;
-        dl[I] = delta;
         c.dmax = fmaxf(c.dmax, fabsf(delta));
         if constexpr (I + 1 < SB)
             sub_update<I>(p, jr, delta, std::make_integer_sequence<int, SB / 4 - ((I + 1) & ~3) / 4>{});
+        if constexpr (NEXT) {
+            // this spin's contribution to the next sub-block's fields (right-looking, off the chain)
+#pragma unroll
+            for (int g = 0; g < SB / 4; ++g) {
+                cn[2 * g] = ffma2(make_float2(jn[g].x, jn[g].y), delta, cn[2 * g]);
+                cn[2 * g + 1] = ffma2(make_float2(jn[g].z, jn[g].w), delta, cn[2 * g + 1]);
+            }
+        }
     } else {
         nv[I] = old[I];
-        dl[I] = 0.0f;
     }
 }
 
-template <bool FULL, bool HAS_H, int... I>
-__device__ __forceinline__ void sub_walk(float2 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB],
-                                         float (&dl)[SB], int k0, SubCtx& c, std::integer_sequence<int, I...>) {
-    (sub_step<I, FULL, HAS_H>(p, old, nv, dl, k0, c), ...);
+template <bool FULL, bool HAS_H, bool NEXT, int... I>
+__device__ __forceinline__ void sub_walk(float2 (&p)[SB / 2], float2 (&cn)[SB / 2], const float (&old)[SB],
+                                         float (&nv)[SB], int k0, SubCtx& c, std::integer_sequence<int, I...>) {
+    (sub_step<I, FULL, HAS_H, NEXT>(p, cn, old, nv, k0, c), ...);
 }
 
 template <bool HAS_H>
-__device__ __forceinline__ void walk_dispatch(float2 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB],
-                                              float (&dl)[SB], int k0, SubCtx& c) {
-    if (k0 + SB <= c.lim)
-        sub_walk<true, HAS_H>(p, old, nv, dl, k0, c, std::make_integer_sequence<int, SB>{});
-    else
-        sub_walk<false, HAS_H>(p, old, nv, dl, k0, c, std::make_integer_sequence<int, SB>{});
+__device__ __forceinline__ void walk_dispatch(float2 (&p)[SB / 2], float2 (&cn)[SB / 2], const float (&old)[SB],
+                                              float (&nv)[SB], int k0, bool next, SubCtx& c) {
+    constexpr auto seq = std::make_integer_sequence<int, SB>{};
+    if (k0 + SB <= c.lim) {
+        if (next) sub_walk<true, HAS_H, true>(p, cn, old, nv, k0, c, seq);
+        else sub_walk<true, HAS_H, false>(p, cn, old, nv, k0, c, seq);
+    } else {
+        sub_walk<false, HAS_H, false>(p, cn, old, nv, k0, c, seq);
+    }
 }
 
 // fields of sub-block k0 += J[j][k0..k0+SB) * Delta_j for the 16 spins j of sub-block `sb`
@@ -517,49 +531,72 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
 
                 for (int s = side; s < NSB; s += 2) {
                     const int k0 = s * SB;
-                    float old[SB], nv[SB], dl[SB];
+                    const bool walk = walkers && s < nsub;
+                    const bool next = walk && s + 1 < nsub;
+                    float old[SB], nv[SB];
                     load_old16(hi_row + b0 + k0, lo_row + b0 + k0, old);
                     float2 pf[SB / 2];
-                    long long tp = 0;
-                    if (walkers && s < nsub) {
-                        // ---- Gauss-Seidel walk of sub-block s (warp-uniform; lanes of
-                        // inactive slots compute but their results are discarded)
-                        float pv[SB];
-                        tmem_ld16(tacc + k0, pv);
 #pragma unroll
-                        for (int j = 0; j < SB / 2; ++j) pf[j] = make_float2(pv[2 * j], pv[2 * j + 1]);
-                        tp = clock64();
+                    for (int j = 0; j < SB / 2; ++j) pf[j] = make_float2(0.0f, 0.0f);
+                    long long tp = clock64();
+                    // ---- fields of sub-block s, part 1: the Delta of sub-blocks < s-1 (final
+                    // while the partner is still walking s-1) -- warp-uniform; lanes of
+                    // inactive slots compute but their results are discarded
+                    if (walk)
                         for (int sb = 0; sb + 1 < s; ++sb) apply_deltas(pf, Jtri, tdel, sb, k0);
-                    }
                     if (s == NSB - 1 && nsub == NSB) {
                         // every warp is past its reads of triangle rows [0, 96) (side 0 has
                         // finished sub-block 6, side 1 its pass over sub-blocks < 6): prefetch the
                         // next block's rows into them (side 1, all of its threads)
                         asm volatile("bar.sync 10, 256;\n" ::: "memory");
                         load_tri_rows(Jtri, a.J32, np, ((b + 1) % nb) * TB, 0, 6 * SB, tside, TM);
-                        tri_prefetched = true;
                     }
-                    if (walkers && s < nsub) {
+                    if (walk) {
+                        const long long ta = clock64();
+                        c_pass0 += ta - tp;
                         if (s > 0) {
-                            const long long ta = clock64();
-                            c_pass0 += ta - tp;
+                            // part 2: the partner folded sub-block s-1's Delta into our
+                            // accumulator columns while it walked; wait for the hand-off
                             asm volatile("bar.sync %0, 64;\n" ::"r"(pair_bar + ((s - 1) & 1)) : "memory");
                             tc_fence_after();
-                            tp = clock64();
-                            c_hand += tp - ta;
-                            apply_deltas(pf, Jtri, tdel, s - 1, k0);
                         }
                         const long long tw = clock64();
-                        if (s > 0) c_pass1 += tw - tp; else c_pass0 += tw - tp;
-                        if (ctx.h) walk_dispatch<true>(pf, old, nv, dl, k0, ctx);
-                        else walk_dispatch<false>(pf, old, nv, dl, k0, ctx);
+                        c_hand += tw - ta;
+                        float pv[SB];
+                        tmem_ld16(tacc + k0, pv);
+#pragma unroll
+                        for (int j = 0; j < SB / 2; ++j) {
+                            pf[j].x += pv[2 * j];
+                            pf[j].y += pv[2 * j + 1];
+                        }
+                        // ---- Gauss-Seidel walk of sub-block s; also accumulates this
+                        // sub-block's contribution to the next one's fields (cn)
+                        float2 cn[SB / 2];
+#pragma unroll
+                        for (int j = 0; j < SB / 2; ++j) cn[j] = make_float2(0.0f, 0.0f);
+                        if (ctx.h) walk_dispatch<true>(pf, cn, old, nv, k0, next, ctx);
+                        else walk_dispatch<false>(pf, cn, old, nv, k0, next, ctx);
                         c_walk += clock64() - tw;
                         ++n_walks;
-                        // Delta history for the later sub-blocks (TMEM, this slot's lane)
+                        // Delta history (TMEM, this slot's lane) and the next sub-block's fields
                         std::uint32_t du[SB];
 #pragma unroll
-                        for (int i = 0; i < SB; ++i) du[i] = __float_as_uint(active ? dl[i] : 0.0f);
+                        for (int i = 0; i < SB; ++i) du[i] = __float_as_uint(active ? nv[i] - old[i] : 0.0f);
                         tmem_st16(tdel + k0, du);
+                        if (next) {
+                            float av[SB];
+                            tmem_ld16(tacc + k0 + SB, av);
+                            std::uint32_t au[SB];
+#pragma unroll
+                            for (int j = 0; j < SB / 2; ++j) {
+                                au[2 * j] = __float_as_uint(av[2 * j] + cn[j].x);
+                                au[2 * j + 1] = __float_as_uint(av[2 * j + 1] + cn[j].y);
+                            }
+                            tmem_st16(tacc + k0 + SB, au);
+                        }
+                        tmem_st_wait();
+                        tc_fence_before();
+                        if (next) asm volatile("bar.arrive %0, 64;\n" ::"r"(pair_bar + (s & 1)) : "memory");
                     }
                     // ---- this slot's new state of the sub-block
                     const bool turnover = !active && (mode == kLoading || mode == kDrain);
@@ -569,7 +606,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         for (int i = 0; i < SB; ++i)
                             if (k0 + i < lim) out[i] = old[i] < 0.0f ? -1 : 1;
                     }
-                    if (!(active && walkers && s < nsub)) {
+                    if (!(active && walk)) {
 #pragma unroll
                         for (int i = 0; i < SB; ++i) nv[i] = old[i];
                     }
@@ -582,8 +619,6 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                                 lane_base + TM_AHI + s * (SB / 2), lane_base + TM_ALO + s * (SB / 2), nv);
                     tmem_st_wait();
                     tc_fence_before();
-                    if (walkers && s + 1 < nsub)
-                        asm volatile("bar.arrive %0, 64;\n" ::"r"(pair_bar + (s & 1)) : "memory");
                     mbar_arrive(&ctl.asub[s]);                 // tail A ready for GEMM(b+1)
                     if (side == 0 && s == NSB - 2 && nsub == NSB)
                         asm volatile("bar.sync 10, 256;\n" ::: "memory");
