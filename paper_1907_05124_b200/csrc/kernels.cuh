@@ -20,10 +20,6 @@ struct RelaxArgs {
     int np;            // padded spins (multiple of the kernel's block size)
     // dense couplings, fp32 row-major [np][np], zero padded
     const float* J32;
-    // CSR couplings (neighbours sorted ascending, model.cpp:116-127), fp64 weights
-    const int* off;
-    const int* idx;
-    const double* w64;
     const float* h32;          // [n] external field, or nullptr (fp32 kernels)
     const double* h64;         // [n] external field, or nullptr (fp64 kernels)
     // the runs of this launch
@@ -91,9 +87,27 @@ int relax_dense_umma_slots_per_cta();
 int relax_dense_umma_block();
 std::size_t relax_dense_umma_plane_rows(int grid);
 
-cudaError_t launch_relax_csr(const RelaxArgs& a, int grid, cudaStream_t st);
-int relax_csr_slots_per_cta();
-std::size_t relax_csr_work_bytes(int np);
+// Level-scheduled sparse kernel (relax_csr.cu).  Spins grouped by Gauss-Seidel level,
+// levels cut into 32-spin chunks, each chunk's neighbour lists interleaved [k][32].
+struct SparseLevels {
+    int nlev;
+    const int* lvl_chunk;      // [nlev + 1] first chunk of each level
+    const int* chunk_base;     // [nchunks] offset of the chunk's [md][32] neighbour block
+    const int* chunk_md;       // [nchunks] longest neighbour list in the chunk
+    const int* spin;           // [nchunks * 32] spin of each lane, -1 for padding
+    const int* nidx;           // interleaved neighbour indices (n = the +0.0 padding slot);
+                               //  unit couplings carry the weight's sign in bit 31
+    const double* nw;          // interleaved weights (non-unit couplings), padding 0.0
+    bool unit;                 // every |J_ij| == 1
+};
+struct SparseLaunch {
+    int grid;
+    int warps;                 // warps per CTA (one run slot per CTA)
+    bool smem_state;           // state in shared memory ([n+1] doubles) or a global row
+};
+cudaError_t launch_relax_sparse(const RelaxArgs& a, const SparseLevels& g, const SparseLaunch& l,
+                                cudaStream_t st);
+int relax_sparse_occupancy(const SparseLaunch& l, bool unit, int n);
 
 cudaError_t launch_energy(const EnergyArgs& a, cudaStream_t st);
 cudaError_t launch_best(const BestArgs& a, int grid, cudaStream_t st);

@@ -125,10 +125,15 @@ struct mars_problem {
     int* dOff = nullptr;            // CSR of the reference storage (exact energy)
     int* dIdx = nullptr;
     double* dW64 = nullptr;
-    int* rOff = nullptr;            // CSR the relaxation kernel walks (aliases dOff/... for
-    int* rIdx = nullptr;            //  adjacency storage; built from the nonzeros otherwise)
-    double* rW64 = nullptr;
-    bool r_owned = false;
+    // level-scheduled sparse relaxation layout (relax_csr.cu), built from the sorted nonzeros
+    int nlev = 0, nchunks = 0, max_level_chunks = 0;
+    bool unit = false;              // every |J_ij| == 1
+    int* dLvlChunk = nullptr;
+    int* dChunkBase = nullptr;
+    int* dChunkMd = nullptr;
+    int* dSpin = nullptr;
+    int* dNIdx = nullptr;
+    double* dNW = nullptr;
     float* dH32 = nullptr;
     double* dH64 = nullptr;
     __half* dJhi = nullptr;         // [np][np] fp16 split of J (tcgen05 kernel)
@@ -145,11 +150,12 @@ struct mars_problem {
         cudaFree(dOff);
         cudaFree(dIdx);
         cudaFree(dW64);
-        if (r_owned) {
-            cudaFree(rOff);
-            cudaFree(rIdx);
-            cudaFree(rW64);
-        }
+        cudaFree(dLvlChunk);
+        cudaFree(dChunkBase);
+        cudaFree(dChunkMd);
+        cudaFree(dSpin);
+        cudaFree(dNIdx);
+        cudaFree(dNW);
         cudaFree(dH32);
         cudaFree(dH64);
         if (stream) cudaStreamDestroy(stream);
@@ -205,6 +211,72 @@ int resolve_kernel(mars_problem* p, int requested) {
         requested == MARS_KERNEL_DENSE_UMMA)
         return requested;
     return -1;
+}
+
+// Gauss-Seidel levels of the ascending sweep (relax_csr.cu): level(i) = 1 + max level of
+// the lower neighbours.  Each level is cut into 32-spin chunks; chunk c's neighbour lists are
+// stored interleaved, entry k of lane l at chunk_base[c] + 32k + l, padded to the chunk's
+// longest list with the +0.0 slot n (weight 0.0).
+int build_levels(mars_problem* p, const std::vector<int>& off, const std::vector<int>& idx,
+                 const std::vector<double>& w) {
+    const int n = p->n;
+    p->np = n + 1;
+    std::vector<int> level(n, 0);
+    int nlev = 1;
+    p->unit = true;
+    for (int i = 0; i < n; ++i) {
+        int l = 0;
+        for (int k = off[i]; k < off[i + 1]; ++k) {
+            if (idx[k] < i) l = std::max(l, level[idx[k]] + 1);
+            if (w[k] != 1.0 && w[k] != -1.0) p->unit = false;
+        }
+        level[i] = l;
+        nlev = std::max(nlev, l + 1);
+    }
+    std::vector<std::vector<int>> by_level(nlev);
+    for (int i = 0; i < n; ++i) by_level[level[i]].push_back(i);
+    std::vector<int> lvl_chunk{0}, chunk_base, chunk_md, spin, nidx;
+    std::vector<double> nw;
+    int max_chunks = 0;
+    for (const auto& members : by_level) {
+        const int chunks = static_cast<int>((members.size() + 31) / 32);
+        max_chunks = std::max(max_chunks, chunks);
+        for (int c = 0; c < chunks; ++c) {
+            int md = 0;
+            for (int l = 0; l < 32; ++l) {
+                const std::size_t m = static_cast<std::size_t>(c) * 32 + l;
+                const int sp = m < members.size() ? members[m] : -1;
+                spin.push_back(sp);
+                if (sp >= 0) md = std::max(md, off[sp + 1] - off[sp]);
+            }
+            chunk_base.push_back(static_cast<int>(nidx.size()));
+            chunk_md.push_back(md);
+            const int* lanes = spin.data() + spin.size() - 32;
+            for (int k = 0; k < md; ++k)
+                for (int l = 0; l < 32; ++l) {
+                    const int sp = lanes[l];
+                    const bool real = sp >= 0 && k < off[sp + 1] - off[sp];
+                    const int e = real ? off[sp] + k : -1;
+                    int code = real ? idx[e] : n;
+                    if (p->unit && real && w[e] < 0.0) code |= static_cast<int>(0x80000000u);
+                    nidx.push_back(code);
+                    if (!p->unit) nw.push_back(real ? w[e] : 0.0);
+                }
+        }
+        lvl_chunk.push_back(static_cast<int>(chunk_md.size()));
+    }
+    if (nidx.size() > 0x7fffffffu) return fail(MARS_ERR_INPUT, "sparse layout exceeds 2^31 entries");
+    p->nlev = nlev;
+    p->nchunks = static_cast<int>(chunk_md.size());
+    p->max_level_chunks = max_chunks;
+    if (int rc = upload(&p->dLvlChunk, lvl_chunk.data(), lvl_chunk.size())) return rc;
+    if (int rc = upload(&p->dChunkBase, chunk_base.data(), chunk_base.size())) return rc;
+    if (int rc = upload(&p->dChunkMd, chunk_md.data(), chunk_md.size())) return rc;
+    if (int rc = upload(&p->dSpin, spin.data(), spin.size())) return rc;
+    if (int rc = upload(&p->dNIdx, nidx.data(), nidx.size())) return rc;
+    if (!p->unit)
+        if (int rc = upload(&p->dNW, nw.data(), nw.size())) return rc;
+    return MARS_OK;
 }
 
 // Device copies in the layouts the kernels use.
@@ -268,10 +340,12 @@ int build_device_store(mars_problem* p) {
                 return fail(MARS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the coupling planes");
         }
     } else {
-        p->np = n;
-        if (p->dense) {  // CSR view of a dense store, ascending columns (row_dot order minus zeros)
-            std::vector<int> off(n + 1, 0), idx;
-            std::vector<double> w64;
+        // relaxation CSR: the reference's sorted adjacency, or the nonzeros of a dense store in
+        // ascending columns (row_dot order minus zero terms, which add nothing: acc is never -0)
+        std::vector<int> off, idx;
+        std::vector<double> w64;
+        if (p->dense) {
+            off.assign(n + 1, 0);
             for (int i = 0; i < n; ++i) {
                 for (int j = 0; j < n; ++j) {
                     const double w = p->J[static_cast<std::size_t>(i) * n + j];
@@ -282,15 +356,9 @@ int build_device_store(mars_problem* p) {
                 }
                 off[i + 1] = static_cast<int>(idx.size());
             }
-            p->r_owned = true;
-            if (int rc = upload(&p->rOff, off.data(), off.size())) return rc;
-            if (int rc = upload(&p->rIdx, idx.data(), idx.size())) return rc;
-            if (int rc = upload(&p->rW64, w64.data(), w64.size())) return rc;
-        } else {
-            p->rOff = p->dOff;
-            p->rIdx = p->dIdx;
-            p->rW64 = p->dW64;
         }
+        if (int rc = build_levels(p, p->dense ? off : p->off, p->dense ? idx : p->idx, p->dense ? w64 : p->wt))
+            return rc;
     }
     return MARS_OK;
 }
@@ -351,6 +419,7 @@ struct mars_batch {
     int best_grid = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     UmmaLaunch umma{};
+    SparseLaunch sparse{};
 
     ~mars_batch() {
         if (!p) return;
@@ -379,6 +448,46 @@ struct mars_batch {
 };
 
 namespace {
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
+
+// Launch shape of the level-scheduled sparse kernel: one run slot per CTA.  State in shared
+// memory when [n+1] doubles fit (else a global row, kept L2-resident by bounding the grid);
+// warps per CTA from the level widths.  MARS_SPARSE_STATE=smem|global, MARS_SPARSE_WARPS and
+// MARS_SPARSE_GRID override (tuning).
+int sparse_config(mars_batch* b) {
+    mars_problem* p = b->p;
+    SparseLaunch& l = b->sparse;
+    const std::size_t state_bytes = static_cast<std::size_t>(p->np) * sizeof(double);
+    l.smem_state = state_bytes <= 200 * 1024;
+    if (const char* v = std::getenv("MARS_SPARSE_STATE")) l.smem_state = std::string(v) != "global" && state_bytes <= 220 * 1024;
+    const double avg = static_cast<double>(p->nchunks) / std::max(p->nlev, 1);
+    int warps = std::max(1, std::min(16, static_cast<int>(std::ceil(avg))));
+    if (l.smem_state) {
+        // few slots per SM: widen the CTA toward the widest level so the SM has work in flight
+        const int per_sm = std::max<int>(1, static_cast<int>((220 * 1024) / (state_bytes + 1024)));
+        while (per_sm * warps < 16 && warps < std::min(32, p->max_level_chunks)) warps *= 2;
+        warps = std::min(warps, 32);
+    }
+    l.warps = std::max(1, std::min(32, env_int("MARS_SPARSE_WARPS", warps)));
+    const int occ = relax_sparse_occupancy(l, p->unit, p->n);
+    if (occ <= 0) return fail(MARS_ERR_CUDA, "sparse kernel does not fit on the device (n = " + std::to_string(p->n) + ")");
+    int grid = occ * p->num_sms;
+    if (!l.smem_state) {
+        // keep the live state rows within ~80 MB of L2
+        const int l2_rows = static_cast<int>((80ull << 20) / state_bytes);
+        grid = std::min(grid, std::max(p->num_sms, l2_rows / p->num_sms * p->num_sms));
+    }
+    l.grid = std::max(1, env_int("MARS_SPARSE_GRID", grid));
+    return MARS_OK;
+}
+
+SparseLevels sparse_levels(const mars_problem* p) {
+    return SparseLevels{p->nlev, p->dLvlChunk, p->dChunkBase, p->dChunkMd, p->dSpin, p->dNIdx, p->dNW, p->unit};
+}
 
 int batch_alloc(mars_batch* b) {
     mars_problem* p = b->p;
@@ -439,14 +548,16 @@ int batch_alloc(mars_batch* b) {
         tm = relax_dense_umma_slots_per_cta();
         per_cta = static_cast<std::size_t>(2) * tm * p->np * sizeof(__half);   // S_hi + S_lo rows
     } else {
-        tm = relax_csr_slots_per_cta();
-        per_cta = relax_csr_work_bytes(p->np);
-        max_grid = 8 * p->num_sms;
+        if (int rc = sparse_config(b)) return rc;
+        tm = 1;
+        max_grid = b->sparse.grid;
+        per_cta = b->sparse.smem_state ? 0 : static_cast<std::size_t>(p->np) * sizeof(double);
     }
     b->grid = std::max(1, std::min(max_grid, (b->queue_len + tm - 1) / tm));
+    b->sparse.grid = b->grid;
     b->slots = b->grid * tm;
     b->work_bytes = per_cta * b->grid;
-    CUDA_TRY(cudaMalloc(&b->d_work, b->work_bytes));
+    CUDA_TRY(cudaMalloc(&b->d_work, std::max<std::size_t>(b->work_bytes, 16)));
     if (p->kernel == MARS_KERNEL_DENSE_UMMA) {
         const std::size_t rows = relax_dense_umma_plane_rows(b->grid);
         b->umma.s_hi = static_cast<__half*>(b->d_work);
@@ -703,9 +814,6 @@ int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
     ra.n = p->n;
     ra.np = p->np;
     ra.J32 = p->dJ32;
-    ra.off = p->rOff;
-    ra.idx = p->rIdx;
-    ra.w64 = p->rW64;
     ra.h32 = p->dH32;
     ra.h64 = p->dH64;
     ra.queue_len = b->queue_len;
@@ -737,7 +845,7 @@ int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
         else if (p->kernel == MARS_KERNEL_DENSE_UMMA)
             CUDA_TRY(launch_relax_dense_umma(ra, b->umma, b->grid, st));
         else
-            CUDA_TRY(launch_relax_csr(ra, b->grid, st));
+            CUDA_TRY(launch_relax_sparse(ra, sparse_levels(p), b->sparse, st));
         ++launches;
     }
     CUDA_TRY(cudaEventRecord(b->ev[1], st));
