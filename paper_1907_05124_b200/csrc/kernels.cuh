@@ -88,26 +88,46 @@ int relax_dense_umma_block();
 std::size_t relax_dense_umma_plane_rows(int grid);
 
 // Level-scheduled sparse kernel (relax_csr.cu).  Spins grouped by Gauss-Seidel level,
-// levels cut into 32-spin chunks, each chunk's neighbour lists interleaved [k][32].
+// levels cut into cw-spin chunks, each chunk's neighbour lists interleaved [k][cw].
 struct SparseLevels {
     int nlev;
     const int* lvl_chunk;      // [nlev + 1] first chunk of each level
-    const int* chunk_base;     // [nchunks] offset of the chunk's [md][32] neighbour block
-    const int* chunk_md;       // [nchunks] longest neighbour list in the chunk
-    const int* spin;           // [nchunks * 32] spin of each lane, -1 for padding
-    const int* nidx;           // interleaved neighbour indices (n = the +0.0 padding slot);
-                               //  unit couplings carry the weight's sign in bit 31
-    const double* nw;          // interleaved weights (non-unit couplings), padding 0.0
+    const int4* ctab;          // [nchunks] {block offset (ints), block length (ints),
+                               //            weight offset (doubles), md}
+    const int* blk;            // chunk blocks: [md,0,0,0][spin x cw (-1 pad)][idx: md x cw]
+                               //  idx n = the +0.0 padding row; unit couplings carry the
+                               //  weight's sign in bit 31
+    const double* wblk;        // non-unit couplings: weight blocks [md x cw], padding 0.0
+    int nchunks;               // chunks per sweep
+    unsigned buf_bytes;        // one chunk buffer in shared memory (16-byte multiple)
+    unsigned wbuf_off;         // weight block offset inside a chunk buffer
     bool unit;                 // every |J_ij| == 1
 };
 struct SparseLaunch {
     int grid;
-    int warps;                 // warps per CTA (one run slot per CTA)
+    int warps;                 // warps per CTA (<= 16)
+    int cw;                    // chunk width (spins per chunk): 32 or 16, as the layout was built
+    int r;                     // runs per lane: 1, 2 or 4; a CTA holds (32/cw)*r run slots
     bool smem_state;           // state in shared memory ([n+1] doubles) or a global row
 };
 cudaError_t launch_relax_sparse(const RelaxArgs& a, const SparseLevels& g, const SparseLaunch& l,
                                 cudaStream_t st);
-int relax_sparse_occupancy(const SparseLaunch& l, bool unit, int n);
+int relax_sparse_occupancy(const SparseLaunch& l, const SparseLevels& g, int n);
+bool relax_sparse_shape_ok(int cw, int r);
+
+// Warp-per-run sparse kernel (relax_spmm.cu): one CTA per SM, `warps` consumer warps each
+// holding 32/cw runs in shared memory, plus a producer warp streaming the chunk blocks
+// through a `ring`-slot TMA ring.
+struct SpmmLaunch {
+    int grid;
+    int warps;
+    int ring;
+    int cw;
+};
+cudaError_t launch_relax_spmm(const RelaxArgs& a, const SparseLevels& g, const SpmmLaunch& l, cudaStream_t st);
+std::size_t relax_spmm_smem(int np, int cw, int warps, int ring, unsigned buf_bytes);
+int relax_spmm_max_warps();
+int relax_spmm_max_ring();
 
 cudaError_t launch_energy(const EnergyArgs& a, cudaStream_t st);
 cudaError_t launch_best(const BestArgs& a, int grid, cudaStream_t st);

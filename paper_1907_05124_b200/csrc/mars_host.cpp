@@ -126,14 +126,13 @@ struct mars_problem {
     int* dIdx = nullptr;
     double* dW64 = nullptr;
     // level-scheduled sparse relaxation layout (relax_csr.cu), built from the sorted nonzeros
-    int nlev = 0, nchunks = 0, max_level_chunks = 0;
+    int nlev = 0, nchunks = 0, max_level_chunks = 0, cw = 32;
     bool unit = false;              // every |J_ij| == 1
+    unsigned buf_bytes = 0, wbuf_off = 0;
     int* dLvlChunk = nullptr;
-    int* dChunkBase = nullptr;
-    int* dChunkMd = nullptr;
-    int* dSpin = nullptr;
-    int* dNIdx = nullptr;
-    double* dNW = nullptr;
+    int4* dCtab = nullptr;
+    int* dBlk = nullptr;
+    double* dWblk = nullptr;
     float* dH32 = nullptr;
     double* dH64 = nullptr;
     __half* dJhi = nullptr;         // [np][np] fp16 split of J (tcgen05 kernel)
@@ -151,11 +150,9 @@ struct mars_problem {
         cudaFree(dIdx);
         cudaFree(dW64);
         cudaFree(dLvlChunk);
-        cudaFree(dChunkBase);
-        cudaFree(dChunkMd);
-        cudaFree(dSpin);
-        cudaFree(dNIdx);
-        cudaFree(dNW);
+        cudaFree(dCtab);
+        cudaFree(dBlk);
+        cudaFree(dWblk);
         cudaFree(dH32);
         cudaFree(dH64);
         if (stream) cudaStreamDestroy(stream);
@@ -235,47 +232,68 @@ int build_levels(mars_problem* p, const std::vector<int>& off, const std::vector
     }
     std::vector<std::vector<int>> by_level(nlev);
     for (int i = 0; i < n; ++i) by_level[level[i]].push_back(i);
-    std::vector<int> lvl_chunk{0}, chunk_base, chunk_md, spin, nidx;
-    std::vector<double> nw;
-    int max_chunks = 0;
+    // within a level the order is free (no couplings): group similar degrees so a chunk's
+    // lanes pad less to its longest list
+    for (auto& m : by_level)
+        std::stable_sort(m.begin(), m.end(), [&](int x, int y) { return off[x + 1] - off[x] > off[y + 1] - off[y]; });
+    // chunk width: 16 when 32-wide chunks would leave most lanes idle (narrow levels)
+    std::size_t chunks32 = 0, chunks16 = 0;
+    for (const auto& m : by_level) {
+        chunks32 += (m.size() + 31) / 32;
+        chunks16 += (m.size() + 15) / 16;
+    }
+    int cw = static_cast<double>(n) / (32.0 * chunks32) < 0.5 && chunks16 < 2 * chunks32 ? 16 : 32;
+    if (const char* v = std::getenv("MARS_SPARSE_CW")) cw = std::atoi(v) == 16 ? 16 : 32;
+    p->cw = cw;
+    // chunk blocks [md,0,0,0][spin x cw][idx: md x cw] (+ weights [md x cw] when non-unit)
+    std::vector<int> lvl_chunk{0}, blk;
+    std::vector<int4> ctab;
+    std::vector<double> wblk;
+    int max_chunks = 0, max_md = 0;
+    std::size_t max_blen = 0;
     for (const auto& members : by_level) {
-        const int chunks = static_cast<int>((members.size() + 31) / 32);
+        const int chunks = static_cast<int>((members.size() + cw - 1) / cw);
         max_chunks = std::max(max_chunks, chunks);
         for (int c = 0; c < chunks; ++c) {
+            int lanes[32];
             int md = 0;
-            for (int l = 0; l < 32; ++l) {
-                const std::size_t m = static_cast<std::size_t>(c) * 32 + l;
-                const int sp = m < members.size() ? members[m] : -1;
-                spin.push_back(sp);
-                if (sp >= 0) md = std::max(md, off[sp + 1] - off[sp]);
+            for (int l = 0; l < cw; ++l) {
+                const std::size_t m = static_cast<std::size_t>(c) * cw + l;
+                lanes[l] = m < members.size() ? members[m] : -1;
+                if (lanes[l] >= 0) md = std::max(md, off[lanes[l] + 1] - off[lanes[l]]);
             }
-            chunk_base.push_back(static_cast<int>(nidx.size()));
-            chunk_md.push_back(md);
-            const int* lanes = spin.data() + spin.size() - 32;
+            const std::size_t boff = blk.size(), woff = wblk.size();
+            blk.insert(blk.end(), {md, 0, 0, 0});
+            blk.insert(blk.end(), lanes, lanes + cw);
             for (int k = 0; k < md; ++k)
-                for (int l = 0; l < 32; ++l) {
+                for (int l = 0; l < cw; ++l) {
                     const int sp = lanes[l];
                     const bool real = sp >= 0 && k < off[sp + 1] - off[sp];
                     const int e = real ? off[sp] + k : -1;
                     int code = real ? idx[e] : n;
                     if (p->unit && real && w[e] < 0.0) code |= static_cast<int>(0x80000000u);
-                    nidx.push_back(code);
-                    if (!p->unit) nw.push_back(real ? w[e] : 0.0);
+                    blk.push_back(code);
+                    if (!p->unit) wblk.push_back(real ? w[e] : 0.0);
                 }
+            const std::size_t blen = blk.size() - boff;
+            if (blk.size() > 0x7fffffffu || wblk.size() > 0x7fffffffu)
+                return fail(MARS_ERR_INPUT, "sparse layout exceeds 2^31 entries");
+            ctab.push_back(make_int4(static_cast<int>(boff), static_cast<int>(blen), static_cast<int>(woff), md));
+            max_blen = std::max(max_blen, blen);
+            max_md = std::max(max_md, md);
         }
-        lvl_chunk.push_back(static_cast<int>(chunk_md.size()));
+        lvl_chunk.push_back(static_cast<int>(ctab.size()));
     }
-    if (nidx.size() > 0x7fffffffu) return fail(MARS_ERR_INPUT, "sparse layout exceeds 2^31 entries");
     p->nlev = nlev;
-    p->nchunks = static_cast<int>(chunk_md.size());
+    p->nchunks = static_cast<int>(ctab.size());
     p->max_level_chunks = max_chunks;
+    p->wbuf_off = static_cast<unsigned>((max_blen * 4 + 15) / 16 * 16);
+    p->buf_bytes = p->wbuf_off + (p->unit ? 0u : static_cast<unsigned>(max_md) * cw * 8u);
     if (int rc = upload(&p->dLvlChunk, lvl_chunk.data(), lvl_chunk.size())) return rc;
-    if (int rc = upload(&p->dChunkBase, chunk_base.data(), chunk_base.size())) return rc;
-    if (int rc = upload(&p->dChunkMd, chunk_md.data(), chunk_md.size())) return rc;
-    if (int rc = upload(&p->dSpin, spin.data(), spin.size())) return rc;
-    if (int rc = upload(&p->dNIdx, nidx.data(), nidx.size())) return rc;
+    if (int rc = upload(&p->dCtab, ctab.data(), ctab.size())) return rc;
+    if (int rc = upload(&p->dBlk, blk.data(), blk.size())) return rc;
     if (!p->unit)
-        if (int rc = upload(&p->dNW, nw.data(), nw.size())) return rc;
+        if (int rc = upload(&p->dWblk, wblk.data(), wblk.size())) return rc;
     return MARS_OK;
 }
 
@@ -420,6 +438,8 @@ struct mars_batch {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     UmmaLaunch umma{};
     SparseLaunch sparse{};
+    SpmmLaunch spmm{};
+    bool use_spmm = false;
 
     ~mars_batch() {
         if (!p) return;
@@ -454,39 +474,74 @@ int env_int(const char* name, int dflt) {
     return v && *v ? std::atoi(v) : dflt;
 }
 
-// Launch shape of the level-scheduled sparse kernel: one run slot per CTA.  State in shared
-// memory when [n+1] doubles fit (else a global row, kept L2-resident by bounding the grid);
-// warps per CTA from the level widths.  MARS_SPARSE_STATE=smem|global, MARS_SPARSE_WARPS and
-// MARS_SPARSE_GRID override (tuning).
+SparseLevels sparse_levels(const mars_problem* p) {
+    return SparseLevels{p->nlev, p->dLvlChunk, p->dCtab, p->dBlk, p->dWblk, p->nchunks, p->buf_bytes, p->wbuf_off, p->unit};
+}
+
+// Launch shape of the level-scheduled sparse kernel.  A CTA relaxes (32/cw)*r runs in
+// lockstep; warps per CTA from the level widths (at most the widest level's chunk count);
+// state in shared memory when it fits beside the warps' chunk buffers (else global rows,
+// kept L2-resident by bounding the grid).  MARS_SPARSE_STATE=smem|global, MARS_SPARSE_R,
+// MARS_SPARSE_WARPS and MARS_SPARSE_GRID override (tuning).
+// Warp-per-run SpMM kernel when its shared memory holds at least 4 consumer warps of runs:
+// RUNS = warps * (32/cw) state rows + a `ring`-slot chunk ring, one CTA per SM.
+// MARS_SPARSE_KERNEL=spmm|levels, MARS_SPMM_WARPS, MARS_SPMM_RING override.
+bool spmm_config(mars_batch* b) {
+    mars_problem* p = b->p;
+    SpmmLaunch& l = b->spmm;
+    const char* k = std::getenv("MARS_SPARSE_KERNEL");
+    if (k && std::string(k) == "levels") return false;
+    constexpr std::size_t kSmem = 220 * 1024;
+    l.cw = p->cw;
+    l.ring = std::max(2, std::min(relax_spmm_max_ring(), env_int("MARS_SPMM_RING", 2)));
+    const std::size_t ring_bytes = static_cast<std::size_t>(l.ring) * p->buf_bytes;
+    const std::size_t warp_bytes = relax_spmm_smem(p->np, l.cw, 1, 0, 0);
+    if (ring_bytes + 4 * warp_bytes > kSmem && !(k && std::string(k) == "spmm")) return false;
+    int warps = static_cast<int>((kSmem - std::min(kSmem, ring_bytes)) / warp_bytes);
+    warps = std::max(1, std::min({relax_spmm_max_warps(), warps, env_int("MARS_SPMM_WARPS", 64)}));
+    const int runs_per_cta = warps * (32 / l.cw);
+    l.warps = warps;
+    l.grid = std::max(1, std::min(p->num_sms, (b->queue_len + runs_per_cta - 1) / runs_per_cta));
+    l.grid = env_int("MARS_SPARSE_GRID", l.grid);
+    return relax_spmm_smem(p->np, l.cw, l.warps, l.ring, p->buf_bytes) <= 227 * 1024;
+}
+
 int sparse_config(mars_batch* b) {
     mars_problem* p = b->p;
     SparseLaunch& l = b->sparse;
-    const std::size_t state_bytes = static_cast<std::size_t>(p->np) * sizeof(double);
-    l.smem_state = state_bytes <= 200 * 1024;
-    if (const char* v = std::getenv("MARS_SPARSE_STATE")) l.smem_state = std::string(v) != "global" && state_bytes <= 220 * 1024;
+    l.cw = p->cw;
+    const int groups = 32 / l.cw;
+    const std::size_t col_bytes = static_cast<std::size_t>(p->np) * sizeof(double);
+    constexpr std::size_t kSmem = 220 * 1024;
+    l.r = env_int("MARS_SPARSE_R", 1);
+    if (!relax_sparse_shape_ok(l.cw, l.r)) return fail(MARS_ERR_INPUT, "MARS_SPARSE_R must be 1, 2 or 4");
+    const int runs = groups * l.r;
+    const std::size_t state_bytes = col_bytes * runs;
     const double avg = static_cast<double>(p->nchunks) / std::max(p->nlev, 1);
     int warps = std::max(1, std::min(16, static_cast<int>(std::ceil(avg))));
+    const auto bufs = [&](int w) { return static_cast<std::size_t>(w) * 2 * p->buf_bytes; };
+    l.smem_state = state_bytes + bufs(warps) <= kSmem;
     if (l.smem_state) {
-        // few slots per SM: widen the CTA toward the widest level so the SM has work in flight
-        const int per_sm = std::max<int>(1, static_cast<int>((220 * 1024) / (state_bytes + 1024)));
-        while (per_sm * warps < 16 && warps < std::min(32, p->max_level_chunks)) warps *= 2;
-        warps = std::min(warps, 32);
+        // few CTAs per SM: widen toward the widest level so the SM has work in flight
+        const int per_sm = std::max<int>(1, static_cast<int>(kSmem / (state_bytes + bufs(warps) + 1024)));
+        while (per_sm * warps < 16 && 2 * warps <= std::min(16, p->max_level_chunks) &&
+               state_bytes + bufs(2 * warps) <= kSmem)
+            warps *= 2;
     }
-    l.warps = std::max(1, std::min(32, env_int("MARS_SPARSE_WARPS", warps)));
-    const int occ = relax_sparse_occupancy(l, p->unit, p->n);
+    // every warp must own a chunk of the widest level (the per-warp chunk streams cycle)
+    l.warps = std::max(1, std::min({16, p->max_level_chunks, env_int("MARS_SPARSE_WARPS", warps)}));
+    if (const char* v = std::getenv("MARS_SPARSE_STATE")) l.smem_state = std::string(v) != "global";
+    if (l.smem_state && state_bytes + bufs(l.warps) > kSmem) l.smem_state = false;
+    const int occ = relax_sparse_occupancy(l, sparse_levels(p), p->n);
     if (occ <= 0) return fail(MARS_ERR_CUDA, "sparse kernel does not fit on the device (n = " + std::to_string(p->n) + ")");
     int grid = occ * p->num_sms;
     if (!l.smem_state) {
         // keep the live state rows within ~80 MB of L2
-        const int l2_rows = static_cast<int>((80ull << 20) / state_bytes);
-        grid = std::min(grid, std::max(p->num_sms, l2_rows / p->num_sms * p->num_sms));
+        const int l2_ctas = static_cast<int>((80ull << 20) / state_bytes);
+        grid = std::min(grid, std::max(p->num_sms, l2_ctas / p->num_sms * p->num_sms));
     }
     l.grid = std::max(1, env_int("MARS_SPARSE_GRID", grid));
     return MARS_OK;
-}
-
-SparseLevels sparse_levels(const mars_problem* p) {
-    return SparseLevels{p->nlev, p->dLvlChunk, p->dChunkBase, p->dChunkMd, p->dSpin, p->dNIdx, p->dNW, p->unit};
 }
 
 int batch_alloc(mars_batch* b) {
@@ -548,13 +603,21 @@ int batch_alloc(mars_batch* b) {
         tm = relax_dense_umma_slots_per_cta();
         per_cta = static_cast<std::size_t>(2) * tm * p->np * sizeof(__half);   // S_hi + S_lo rows
     } else {
-        if (int rc = sparse_config(b)) return rc;
-        tm = 1;
-        max_grid = b->sparse.grid;
-        per_cta = b->sparse.smem_state ? 0 : static_cast<std::size_t>(p->np) * sizeof(double);
+        b->use_spmm = spmm_config(b);
+        if (b->use_spmm) {
+            tm = b->spmm.warps * (32 / b->spmm.cw);
+            max_grid = b->spmm.grid;
+            per_cta = 0;
+        } else {
+            if (int rc = sparse_config(b)) return rc;
+            tm = (32 / b->sparse.cw) * b->sparse.r;
+            max_grid = b->sparse.grid;
+            per_cta = b->sparse.smem_state ? 0 : static_cast<std::size_t>(p->np) * tm * sizeof(double);
+        }
     }
     b->grid = std::max(1, std::min(max_grid, (b->queue_len + tm - 1) / tm));
     b->sparse.grid = b->grid;
+    b->spmm.grid = b->grid;
     b->slots = b->grid * tm;
     b->work_bytes = per_cta * b->grid;
     CUDA_TRY(cudaMalloc(&b->d_work, std::max<std::size_t>(b->work_bytes, 16)));
@@ -845,7 +908,8 @@ int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
         else if (p->kernel == MARS_KERNEL_DENSE_UMMA)
             CUDA_TRY(launch_relax_dense_umma(ra, b->umma, b->grid, st));
         else
-            CUDA_TRY(launch_relax_sparse(ra, sparse_levels(p), b->sparse, st));
+            CUDA_TRY(b->use_spmm ? launch_relax_spmm(ra, sparse_levels(p), b->spmm, st)
+                                 : launch_relax_sparse(ra, sparse_levels(p), b->sparse, st));
         ++launches;
     }
     CUDA_TRY(cudaEventRecord(b->ev[1], st));

@@ -86,6 +86,17 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, st
         : "memory");
 }
 
+// 1D bulk copy global -> shared (TMA engine, no tensor map): `bytes` and both addresses
+// multiples of 16; completes `bytes` of transaction count on `bar`.
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, std::uint32_t bytes,
+                                          std::uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(reinterpret_cast<std::uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // Generic-proxy global writes -> visible to later async-proxy (TMA) reads.
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;\n" ::: "memory");

@@ -234,7 +234,8 @@ def test_workload_prefix_matches_reference(name, frac):
 def test_sparse_launch_shapes_bit_identical(kind, monkeypatch, port):
     """The level-scheduled sparse kernel is the reference's sequential sweep reordered only
     across uncoupled spins: every launch shape (state in shared memory or in a global row,
-    1..8 warps per run, any grid) must give bit-identical records, and those records must
+    1..8 warps, 16- or 32-spin chunks, 1..8 runs per CTA, any grid; or the warp-per-run
+    kernel with any ring depth) must give bit-identical records, and those records must
     match the reference port run for run."""
     if kind == "ea2d":
         n, (u, v, w) = 24 * 24, mb.gen_ea(24, 2, 3)
@@ -249,14 +250,24 @@ def test_sparse_launch_shapes_bit_identical(kind, monkeypatch, port):
         w = rng.standard_normal(u.size)
     spec = mb.BatchSpec(uniform(6), 96, 11, keep_spins=True)
     results = []
-    for state, warps, grid in [("smem", "1", "0"), ("smem", "4", "7"), ("global", "2", "0"),
-                               ("global", "8", "5")]:
-        monkeypatch.setenv("MARS_SPARSE_STATE", state)
-        monkeypatch.setenv("MARS_SPARSE_WARPS", warps)
-        if grid != "0":
-            monkeypatch.setenv("MARS_SPARSE_GRID", grid)
-        else:
-            monkeypatch.delenv("MARS_SPARSE_GRID", raising=False)
+    levels = [("smem", "1", "0", "1", "32"), ("smem", "4", "7", "4", "16"),
+              ("global", "2", "0", "2", "32"), ("global", "8", "5", "4", "32"),
+              ("smem", "2", "0", "2", "16"), ("global", "3", "0", "1", "16")]
+    shapes = [dict(MARS_SPARSE_KERNEL="levels", MARS_SPARSE_STATE=st, MARS_SPARSE_WARPS=wp,
+                   MARS_SPARSE_GRID=gr, MARS_SPARSE_R=r, MARS_SPARSE_CW=cw)
+              for st, wp, gr, r, cw in levels]
+    # warp-per-run kernel: consumer warps x ring depth x chunk width x grid
+    shapes += [dict(MARS_SPARSE_KERNEL="spmm", MARS_SPMM_WARPS=wp, MARS_SPMM_RING=rg,
+                    MARS_SPARSE_CW=cw, MARS_SPARSE_GRID=gr)
+               for wp, rg, cw, gr in [("1", "2", "32", "0"), ("3", "3", "16", "5"),
+                                      ("8", "4", "32", "0"), ("2", "8", "16", "0")]]
+    for env in shapes:
+        for k in ("MARS_SPARSE_KERNEL", "MARS_SPARSE_STATE", "MARS_SPARSE_WARPS", "MARS_SPARSE_GRID",
+                  "MARS_SPARSE_R", "MARS_SPARSE_CW", "MARS_SPMM_WARPS", "MARS_SPMM_RING"):
+            monkeypatch.delenv(k, raising=False)
+        for k, val in env.items():
+            if val != "0":
+                monkeypatch.setenv(k, val)
         p = mb.IsingProblem.from_edges(n, (u, v, w))
         assert p.kernel() == "csr"
         results.append(mb.run_batch(p, spec).records)
