@@ -117,17 +117,18 @@ bool relax_sparse_shape_ok(int cw, int r);
 
 // Warp-per-run sparse kernel (relax_spmm.cu): one CTA per SM, `warps` consumer warps each
 // holding 32/cw runs in shared memory, plus a producer warp streaming the chunk blocks
-// through a `ring`-slot TMA ring.
+// through a `ring_bytes` TMA byte ring (>= the largest block, 16-byte multiple).
 struct SpmmLaunch {
     int grid;
     int warps;
-    int ring;
-    int cw;
+    int ring_bytes;
+    int cw;                    // chunk (layout) width: 16, 32 or 64
+    int h;                     // runs per warp (1 or 2); spins per lane = cw * h / 32 (1 or 2)
 };
 cudaError_t launch_relax_spmm(const RelaxArgs& a, const SparseLevels& g, const SpmmLaunch& l, cudaStream_t st);
-std::size_t relax_spmm_smem(int np, int cw, int warps, int ring, unsigned buf_bytes);
+std::size_t relax_spmm_smem(int np, int runs_per_warp, int warps, int ring_bytes);
 int relax_spmm_max_warps();
-int relax_spmm_max_ring();
+bool relax_spmm_shape_ok(int layout_width, int runs_per_warp);
 
 cudaError_t launch_energy(const EnergyArgs& a, cudaStream_t st);
 cudaError_t launch_best(const BestArgs& a, int grid, cudaStream_t st);

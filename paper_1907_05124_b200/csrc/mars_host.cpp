@@ -129,6 +129,7 @@ struct mars_problem {
     int nlev = 0, nchunks = 0, max_level_chunks = 0, cw = 32;
     bool unit = false;              // every |J_ij| == 1
     unsigned buf_bytes = 0, wbuf_off = 0;
+    std::size_t chunk_bytes = 0;    // all chunk blocks (+ weights), bytes
     int* dLvlChunk = nullptr;
     int4* dCtab = nullptr;
     int* dBlk = nullptr;
@@ -236,14 +237,24 @@ int build_levels(mars_problem* p, const std::vector<int>& off, const std::vector
     // lanes pad less to its longest list
     for (auto& m : by_level)
         std::stable_sort(m.begin(), m.end(), [&](int x, int y) { return off[x + 1] - off[x] > off[y + 1] - off[y]; });
-    // chunk width: 16 when 32-wide chunks would leave most lanes idle (narrow levels)
+    // chunk width.  Warp-per-run kernel (state small enough for >= 4 runs per SM): 16 for
+    // narrow levels (two runs per warp), 64 for wide ones (two spins per lane), else 32.
+    // Level-parallel kernel: 16 when 32-wide chunks would leave most lanes idle, else 32.
     std::size_t chunks32 = 0, chunks16 = 0;
     for (const auto& m : by_level) {
         chunks32 += (m.size() + 31) / 32;
         chunks16 += (m.size() + 15) / 16;
     }
+    const char* kern = std::getenv("MARS_SPARSE_KERNEL");
+    const bool spmm_layout = !(kern && std::string(kern) == "levels") &&
+                             (static_cast<std::size_t>(n) + 1) * sizeof(double) * 4 <= 180 * 1024;
+    const double per_level = static_cast<double>(n) / nlev;
     int cw = static_cast<double>(n) / (32.0 * chunks32) < 0.5 && chunks16 < 2 * chunks32 ? 16 : 32;
-    if (const char* v = std::getenv("MARS_SPARSE_CW")) cw = std::atoi(v) == 16 ? 16 : 32;
+    if (spmm_layout) cw = per_level < 20 ? 16 : 32;   // 64 (two spins per lane) measured slower
+    if (const char* v = std::getenv("MARS_SPARSE_CW")) {
+        const int want = std::atoi(v);
+        cw = want == 16 ? 16 : (want == 64 && spmm_layout ? 64 : 32);
+    }
     p->cw = cw;
     // chunk blocks [md,0,0,0][spin x cw][idx: md x cw] (+ weights [md x cw] when non-unit)
     std::vector<int> lvl_chunk{0}, blk;
@@ -251,20 +262,21 @@ int build_levels(mars_problem* p, const std::vector<int>& off, const std::vector
     std::vector<double> wblk;
     int max_chunks = 0, max_md = 0;
     std::size_t max_blen = 0;
+    std::vector<int> lanes(cw);
     for (const auto& members : by_level) {
         const int chunks = static_cast<int>((members.size() + cw - 1) / cw);
         max_chunks = std::max(max_chunks, chunks);
         for (int c = 0; c < chunks; ++c) {
-            int lanes[32];
             int md = 0;
             for (int l = 0; l < cw; ++l) {
                 const std::size_t m = static_cast<std::size_t>(c) * cw + l;
                 lanes[l] = m < members.size() ? members[m] : -1;
                 if (lanes[l] >= 0) md = std::max(md, off[lanes[l] + 1] - off[lanes[l]]);
             }
+            md = (md + 3) / 4 * 4;   // the warp-per-run kernel gathers in groups of 4
             const std::size_t boff = blk.size(), woff = wblk.size();
             blk.insert(blk.end(), {md, 0, 0, 0});
-            blk.insert(blk.end(), lanes, lanes + cw);
+            blk.insert(blk.end(), lanes.begin(), lanes.end());
             for (int k = 0; k < md; ++k)
                 for (int l = 0; l < cw; ++l) {
                     const int sp = lanes[l];
@@ -287,6 +299,7 @@ int build_levels(mars_problem* p, const std::vector<int>& off, const std::vector
     p->nlev = nlev;
     p->nchunks = static_cast<int>(ctab.size());
     p->max_level_chunks = max_chunks;
+    p->chunk_bytes = blk.size() * 4 + wblk.size() * 8;
     p->wbuf_off = static_cast<unsigned>((max_blen * 4 + 15) / 16 * 16);
     p->buf_bytes = p->wbuf_off + (p->unit ? 0u : static_cast<unsigned>(max_md) * cw * 8u);
     if (int rc = upload(&p->dLvlChunk, lvl_chunk.data(), lvl_chunk.size())) return rc;
@@ -485,7 +498,7 @@ SparseLevels sparse_levels(const mars_problem* p) {
 // MARS_SPARSE_WARPS and MARS_SPARSE_GRID override (tuning).
 // Warp-per-run SpMM kernel when its shared memory holds at least 4 consumer warps of runs:
 // RUNS = warps * (32/cw) state rows + a `ring`-slot chunk ring, one CTA per SM.
-// MARS_SPARSE_KERNEL=spmm|levels, MARS_SPMM_WARPS, MARS_SPMM_RING override.
+// MARS_SPARSE_KERNEL=spmm|levels, MARS_SPMM_WARPS, MARS_SPMM_RING_KB override.
 bool spmm_config(mars_batch* b) {
     mars_problem* p = b->p;
     SpmmLaunch& l = b->spmm;
@@ -493,23 +506,35 @@ bool spmm_config(mars_batch* b) {
     if (k && std::string(k) == "levels") return false;
     constexpr std::size_t kSmem = 220 * 1024;
     l.cw = p->cw;
-    l.ring = std::max(2, std::min(relax_spmm_max_ring(), env_int("MARS_SPMM_RING", 2)));
-    const std::size_t ring_bytes = static_cast<std::size_t>(l.ring) * p->buf_bytes;
-    const std::size_t warp_bytes = relax_spmm_smem(p->np, l.cw, 1, 0, 0);
+    if (l.cw > 32 && k && std::string(k) == "levels") return false;
+    // runs per warp: two 16-lane groups for 16-wide chunks, else one run per warp
+    l.h = env_int("MARS_SPMM_H", l.cw == 16 ? 2 : 1);
+    if (!relax_spmm_shape_ok(l.cw, l.h)) l.h = l.cw == 16 ? 2 : 1;
+    // byte ring: the largest block plus ~3 average blocks in flight (MARS_SPMM_RING_KB)
+    const std::size_t avg = p->nchunks ? p->chunk_bytes / p->nchunks : p->buf_bytes;
+    std::size_t ring_bytes = std::max<std::size_t>(p->buf_bytes + 3 * avg, 2 * p->buf_bytes);
+    if (const int kb = env_int("MARS_SPMM_RING_KB", 0)) ring_bytes = static_cast<std::size_t>(kb) * 1024;
+    ring_bytes = std::max<std::size_t>((ring_bytes + 15) / 16 * 16, p->buf_bytes);
+    l.ring_bytes = static_cast<int>(ring_bytes);
+    const std::size_t warp_bytes = relax_spmm_smem(p->np, l.h, 1, 0);
     if (ring_bytes + 4 * warp_bytes > kSmem && !(k && std::string(k) == "spmm")) return false;
-    int warps = static_cast<int>((kSmem - std::min(kSmem, ring_bytes)) / warp_bytes);
+    // CTAs per SM (each with its own ring): smaller CTAs couple fewer warps to one ring
+    const int per_sm = std::max(1, env_int("MARS_SPMM_CTAS_PER_SM", 1));
+    const std::size_t budget = (kSmem + 1024) / per_sm - 1024;
+    int warps = static_cast<int>((budget - std::min(budget, ring_bytes)) / warp_bytes);
     warps = std::max(1, std::min({relax_spmm_max_warps(), warps, env_int("MARS_SPMM_WARPS", 64)}));
-    const int runs_per_cta = warps * (32 / l.cw);
+    const int runs_per_cta = warps * l.h;
     l.warps = warps;
-    l.grid = std::max(1, std::min(p->num_sms, (b->queue_len + runs_per_cta - 1) / runs_per_cta));
+    l.grid = std::max(1, std::min(per_sm * p->num_sms, (b->queue_len + runs_per_cta - 1) / runs_per_cta));
     l.grid = env_int("MARS_SPARSE_GRID", l.grid);
-    return relax_spmm_smem(p->np, l.cw, l.warps, l.ring, p->buf_bytes) <= 227 * 1024;
+    return relax_spmm_smem(p->np, l.h, l.warps, l.ring_bytes) <= 227 * 1024;
 }
 
 int sparse_config(mars_batch* b) {
     mars_problem* p = b->p;
     SparseLaunch& l = b->sparse;
     l.cw = p->cw;
+    if (l.cw > 32) return fail(MARS_ERR_INPUT, "64-wide chunk layout needs the warp-per-run kernel");
     const int groups = 32 / l.cw;
     const std::size_t col_bytes = static_cast<std::size_t>(p->np) * sizeof(double);
     constexpr std::size_t kSmem = 220 * 1024;
@@ -605,7 +630,7 @@ int batch_alloc(mars_batch* b) {
     } else {
         b->use_spmm = spmm_config(b);
         if (b->use_spmm) {
-            tm = b->spmm.warps * (32 / b->spmm.cw);
+            tm = b->spmm.warps * b->spmm.h;
             max_grid = b->spmm.grid;
             per_cta = 0;
         } else {
@@ -933,6 +958,11 @@ int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
         double acc[kProfSlots] = {0};
         for (int c = 0; c < b->grid; ++c)
             for (int k = 0; k < kProfSlots; ++k) acc[k] += static_cast<double>(h[c * kProfSlots + k]);
+        if (p->kernel == MARS_KERNEL_CSR && b->use_spmm && acc[0] > 0) {
+            const double per = acc[0] * p->nchunks;   // warp-chunks
+            std::fprintf(stderr, "[mars prof] spmm: %.0f warp-sweeps; per warp-chunk: wait %.0f, sum %.0f, trial %.0f cycles\n",
+                         acc[0], acc[1] / per, acc[2] / per, acc[3] / per);
+        }
         const double blocks = acc[0] * (h[6] ? h[6] : 1);
         std::fprintf(stderr,
                      "[mars prof] grid %d: sweeps/cta %.1f, cycles/cta %.3g | per block: loads %.0f, "

@@ -257,16 +257,22 @@ def test_sparse_launch_shapes_bit_identical(kind, monkeypatch, port):
                    MARS_SPARSE_GRID=gr, MARS_SPARSE_R=r, MARS_SPARSE_CW=cw)
               for st, wp, gr, r, cw in levels]
     # warp-per-run kernel: consumer warps x ring depth x chunk width x grid
-    shapes += [dict(MARS_SPARSE_KERNEL="spmm", MARS_SPMM_WARPS=wp, MARS_SPMM_RING=rg,
-                    MARS_SPARSE_CW=cw, MARS_SPARSE_GRID=gr)
-               for wp, rg, cw, gr in [("1", "2", "32", "0"), ("3", "3", "16", "5"),
-                                      ("8", "4", "32", "0"), ("2", "8", "16", "0")]]
+    # (ring sizes from "just the largest block" upward exercise the byte ring's wrap-around)
+    # chunk width x runs per warp covers all four (runs per warp, spins per lane) variants
+    shapes += [dict(MARS_SPARSE_KERNEL="spmm", MARS_SPMM_WARPS=wp, MARS_SPMM_RING_KB=rg,
+                    MARS_SPARSE_CW=cw, MARS_SPMM_H=hh, MARS_SPARSE_GRID=gr)
+               for wp, rg, cw, hh, gr in [("1", "1", "32", "1", "0"), ("3", "3", "16", "2", "5"),
+                                          ("8", "5", "64", "1", "0"), ("2", "40", "32", "2", "0"),
+                                          ("16", "8", "64", "1", "3")]]
     for env in shapes:
         for k in ("MARS_SPARSE_KERNEL", "MARS_SPARSE_STATE", "MARS_SPARSE_WARPS", "MARS_SPARSE_GRID",
-                  "MARS_SPARSE_R", "MARS_SPARSE_CW", "MARS_SPMM_WARPS", "MARS_SPMM_RING"):
+                  "MARS_SPARSE_R", "MARS_SPARSE_CW", "MARS_SPMM_WARPS", "MARS_SPMM_RING_KB",
+                  "MARS_SPMM_H"):
             monkeypatch.delenv(k, raising=False)
         for k, val in env.items():
-            if val != "0":
+            if val == "off":
+                monkeypatch.setenv(k, "0")
+            elif val != "0":
                 monkeypatch.setenv(k, val)
         p = mb.IsingProblem.from_edges(n, (u, v, w))
         assert p.kernel() == "csr"
