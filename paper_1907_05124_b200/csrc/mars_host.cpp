@@ -128,6 +128,12 @@ struct mars_problem {
     // level-scheduled sparse relaxation layout (relax_csr.cu), built from the sorted nonzeros
     int nlev = 0, nchunks = 0, max_level_chunks = 0, cw = 32;
     bool unit = false;              // every |J_ij| == 1
+    // torus stencil layout (relax_stencil.cu), when the adjacency is an L^dims +-1 torus
+    bool stencil = false;
+    int st_dims = 0, st_L = 0, st_nlev = 0, st_maxw = 0;
+    int* dStLvl = nullptr;
+    unsigned* dStCoords = nullptr;
+    unsigned char* dStSigns = nullptr;
     unsigned buf_bytes = 0, wbuf_off = 0;
     std::size_t chunk_bytes = 0;    // all chunk blocks (+ weights), bytes
     int* dLvlChunk = nullptr;
@@ -150,6 +156,9 @@ struct mars_problem {
         cudaFree(dOff);
         cudaFree(dIdx);
         cudaFree(dW64);
+        cudaFree(dStLvl);
+        cudaFree(dStCoords);
+        cudaFree(dStSigns);
         cudaFree(dLvlChunk);
         cudaFree(dCtab);
         cudaFree(dBlk);
@@ -209,6 +218,70 @@ int resolve_kernel(mars_problem* p, int requested) {
         requested == MARS_KERNEL_DENSE_UMMA)
         return requested;
     return -1;
+}
+
+// Torus recognition for the stencil kernel: n = L^dims (dims 2 or 3, 3 <= L <= 1024), every
+// coupling +-1, and every adjacency row exactly the 2*dims lattice neighbours of the site
+// (site i = c0 + L*c1 + L^2*c2, bonds to c_d +- 1 mod L) in ascending order.  Builds the
+// level lists (coordinate sums) and one sign byte per site (bit k: k-th row entry is -1).
+int try_stencil(mars_problem* p, const std::vector<int>& off, const std::vector<int>& idx,
+                const std::vector<double>& w) {
+    const int n = p->n;
+    for (int dims = 2; dims <= 3; ++dims) {
+        const int L = static_cast<int>(std::lround(std::pow(static_cast<double>(n), 1.0 / dims)));
+        std::int64_t nn = 1;
+        for (int d = 0; d < dims; ++d) nn *= L;
+        if (nn != n || L < 3 || L > 1024) continue;
+        std::vector<unsigned char> signs(n, 0);
+        bool ok = true;
+        for (int i = 0; i < n && ok; ++i) {
+            if (off[i + 1] - off[i] != 2 * dims) { ok = false; break; }
+            int nb[6], stride = 1;
+            for (int d = 0; d < dims; ++d) {
+                const int c = (i / stride) % L;
+                nb[2 * d] = c ? i - stride : i + (L - 1) * stride;
+                nb[2 * d + 1] = c < L - 1 ? i + stride : i - (L - 1) * stride;
+                stride *= L;
+            }
+            std::sort(nb, nb + 2 * dims);
+            for (int k = 0; k < 2 * dims; ++k) {
+                const int e = off[i] + k;
+                if (idx[e] != nb[k] || (w[e] != 1.0 && w[e] != -1.0)) { ok = false; break; }
+                if (w[e] < 0.0) signs[i] |= static_cast<unsigned char>(1u << k);
+            }
+        }
+        if (!ok) continue;
+        const int nlev = dims * (L - 1) + 1;
+        std::vector<std::vector<unsigned>> lv(nlev);
+        for (int i = 0; i < n; ++i) {
+            int c[3] = {0, 0, 0}, stride = 1, sum = 0;
+            for (int d = 0; d < dims; ++d) {
+                c[d] = (i / stride) % L;
+                sum += c[d];
+                stride *= L;
+            }
+            lv[sum].push_back(static_cast<unsigned>(c[0]) | static_cast<unsigned>(c[1]) << 10 |
+                              static_cast<unsigned>(c[2]) << 20);
+        }
+        std::vector<int> lvl_off{0};
+        std::vector<unsigned> coords;
+        int maxw = 0;
+        for (const auto& l : lv) {
+            coords.insert(coords.end(), l.begin(), l.end());
+            lvl_off.push_back(static_cast<int>(coords.size()));
+            maxw = std::max(maxw, static_cast<int>(l.size()));
+        }
+        if (int rc = upload(&p->dStLvl, lvl_off.data(), lvl_off.size())) return rc;
+        if (int rc = upload(&p->dStCoords, coords.data(), coords.size())) return rc;
+        if (int rc = upload(&p->dStSigns, signs.data(), signs.size())) return rc;
+        p->stencil = true;
+        p->st_dims = dims;
+        p->st_L = L;
+        p->st_nlev = nlev;
+        p->st_maxw = maxw;
+        return MARS_OK;
+    }
+    return MARS_OK;
 }
 
 // Gauss-Seidel levels of the ascending sweep (relax_csr.cu): level(i) = 1 + max level of
@@ -390,6 +463,8 @@ int build_device_store(mars_problem* p) {
         }
         if (int rc = build_levels(p, p->dense ? off : p->off, p->dense ? idx : p->idx, p->dense ? w64 : p->wt))
             return rc;
+        if (int rc = try_stencil(p, p->dense ? off : p->off, p->dense ? idx : p->idx, p->dense ? w64 : p->wt))
+            return rc;
     }
     return MARS_OK;
 }
@@ -453,6 +528,8 @@ struct mars_batch {
     SparseLaunch sparse{};
     SpmmLaunch spmm{};
     bool use_spmm = false;
+    StencilLaunch stencil{};
+    bool use_stencil = false;
 
     ~mars_batch() {
         if (!p) return;
@@ -628,8 +705,20 @@ int batch_alloc(mars_batch* b) {
         tm = relax_dense_umma_slots_per_cta();
         per_cta = static_cast<std::size_t>(2) * tm * p->np * sizeof(__half);   // S_hi + S_lo rows
     } else {
-        b->use_spmm = spmm_config(b);
-        if (b->use_spmm) {
+        const char* kk = std::getenv("MARS_SPARSE_KERNEL");
+        b->use_stencil = p->stencil && !(kk && std::string(kk) != "stencil");
+        if (b->use_stencil) {
+            // one run per CTA; state in shared memory when it fits beside the sign bytes
+            StencilLaunch& l = b->stencil;
+            l.smem_state = relax_stencil_smem(p->n, true) <= 220 * 1024;
+            if (const char* v = std::getenv("MARS_SPARSE_STATE")) l.smem_state = l.smem_state && std::string(v) != "global";
+            l.threads = std::min(1024, std::max(32, (p->st_maxw + 31) / 32 * 32));
+            l.threads = std::max(32, std::min(1024, env_int("MARS_STENCIL_THREADS", l.threads)) / 32 * 32);
+            const int per_sm = l.smem_state ? 1 : std::max(1, env_int("MARS_STENCIL_CTAS_PER_SM", 1));
+            tm = 1;
+            max_grid = env_int("MARS_SPARSE_GRID", per_sm * p->num_sms);
+            per_cta = l.smem_state ? 0 : static_cast<std::size_t>(p->np) * sizeof(double);
+        } else if ((b->use_spmm = spmm_config(b))) {
             tm = b->spmm.warps * b->spmm.h;
             max_grid = b->spmm.grid;
             per_cta = 0;
@@ -643,6 +732,7 @@ int batch_alloc(mars_batch* b) {
     b->grid = std::max(1, std::min(max_grid, (b->queue_len + tm - 1) / tm));
     b->sparse.grid = b->grid;
     b->spmm.grid = b->grid;
+    b->stencil.grid = b->grid;
     b->slots = b->grid * tm;
     b->work_bytes = per_cta * b->grid;
     CUDA_TRY(cudaMalloc(&b->d_work, std::max<std::size_t>(b->work_bytes, 16)));
@@ -933,8 +1023,11 @@ int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
         else if (p->kernel == MARS_KERNEL_DENSE_UMMA)
             CUDA_TRY(launch_relax_dense_umma(ra, b->umma, b->grid, st));
         else
-            CUDA_TRY(b->use_spmm ? launch_relax_spmm(ra, sparse_levels(p), b->spmm, st)
-                                 : launch_relax_sparse(ra, sparse_levels(p), b->sparse, st));
+            CUDA_TRY(b->use_stencil
+                         ? launch_relax_stencil(ra, StencilArgs{p->st_dims, p->st_L, p->st_nlev, p->dStLvl, p->dStCoords, p->dStSigns},
+                                                b->stencil, st)
+                         : b->use_spmm ? launch_relax_spmm(ra, sparse_levels(p), b->spmm, st)
+                                       : launch_relax_sparse(ra, sparse_levels(p), b->sparse, st));
         ++launches;
     }
     CUDA_TRY(cudaEventRecord(b->ev[1], st));

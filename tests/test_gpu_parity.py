@@ -264,8 +264,14 @@ def test_sparse_launch_shapes_bit_identical(kind, monkeypatch, port):
                for wp, rg, cw, hh, gr in [("1", "1", "32", "1", "0"), ("3", "3", "16", "2", "5"),
                                           ("8", "5", "64", "1", "0"), ("2", "40", "32", "2", "0"),
                                           ("16", "8", "64", "1", "3")]]
+    if kind != "er_gauss":
+        # torus stencil kernel: state in shared memory or a global row, any CTA width / grid
+        shapes += [dict(MARS_SPARSE_KERNEL="stencil", MARS_SPARSE_STATE=st, MARS_STENCIL_THREADS=th,
+                        MARS_SPARSE_GRID=gr)
+                   for st, th, gr in [("smem", "0", "0"), ("global", "64", "3"), ("smem", "32", "0"),
+                                      ("global", "1024", "0")]]
     for env in shapes:
-        for k in ("MARS_SPARSE_KERNEL", "MARS_SPARSE_STATE", "MARS_SPARSE_WARPS", "MARS_SPARSE_GRID",
+        for k in ("MARS_SPARSE_KERNEL", "MARS_STENCIL_THREADS", "MARS_SPARSE_STATE", "MARS_SPARSE_WARPS", "MARS_SPARSE_GRID",
                   "MARS_SPARSE_R", "MARS_SPARSE_CW", "MARS_SPMM_WARPS", "MARS_SPMM_RING_KB",
                   "MARS_SPMM_H"):
             monkeypatch.delenv(k, raising=False)
