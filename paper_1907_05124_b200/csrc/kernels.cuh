@@ -133,11 +133,11 @@ bool relax_spmm_shape_ok(int layout_width, int runs_per_warp);
 // Torus stencil kernel (relax_stencil.cu): L^dims lattice with unit couplings.
 struct StencilArgs {
     int dims;                  // 2 or 3
-    int L;                     // side (3..1024)
+    int L;                     // side (3..256)
     int nlev;                  // dims*(L-1)+1 Gauss-Seidel levels (coordinate sums)
     const int* lvl_off;        // [nlev + 1] first site of each level in `coords`
-    const unsigned* coords;    // [n] sites by level: c0 | c1 << 10 | c2 << 20
-    const unsigned char* signs;// [n] bit k = the k-th smallest neighbour's coupling is -1
+    const unsigned* coords;    // [n] sites by level: c0 | c1 << 8 | c2 << 16 | signs << 24,
+                               //  sign bit k = the k-th smallest neighbour's coupling is -1
 };
 struct StencilLaunch {
     int grid;
@@ -145,7 +145,7 @@ struct StencilLaunch {
     bool smem_state;           // state in shared memory, else a global row per CTA
 };
 cudaError_t launch_relax_stencil(const RelaxArgs& a, const StencilArgs& g, const StencilLaunch& l, cudaStream_t st);
-std::size_t relax_stencil_smem(int n, bool smem_state);
+std::size_t relax_stencil_smem(int n, int nlev, bool smem_state);
 
 cudaError_t launch_energy(const EnergyArgs& a, cudaStream_t st);
 cudaError_t launch_best(const BestArgs& a, int grid, cudaStream_t st);

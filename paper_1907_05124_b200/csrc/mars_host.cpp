@@ -133,7 +133,6 @@ struct mars_problem {
     int st_dims = 0, st_L = 0, st_nlev = 0, st_maxw = 0;
     int* dStLvl = nullptr;
     unsigned* dStCoords = nullptr;
-    unsigned char* dStSigns = nullptr;
     unsigned buf_bytes = 0, wbuf_off = 0;
     std::size_t chunk_bytes = 0;    // all chunk blocks (+ weights), bytes
     int* dLvlChunk = nullptr;
@@ -158,7 +157,6 @@ struct mars_problem {
         cudaFree(dW64);
         cudaFree(dStLvl);
         cudaFree(dStCoords);
-        cudaFree(dStSigns);
         cudaFree(dLvlChunk);
         cudaFree(dCtab);
         cudaFree(dBlk);
@@ -220,7 +218,7 @@ int resolve_kernel(mars_problem* p, int requested) {
     return -1;
 }
 
-// Torus recognition for the stencil kernel: n = L^dims (dims 2 or 3, 3 <= L <= 1024), every
+// Torus recognition for the stencil kernel: n = L^dims (dims 2 or 3, 3 <= L <= 256), every
 // coupling +-1, and every adjacency row exactly the 2*dims lattice neighbours of the site
 // (site i = c0 + L*c1 + L^2*c2, bonds to c_d +- 1 mod L) in ascending order.  Builds the
 // level lists (coordinate sums) and one sign byte per site (bit k: k-th row entry is -1).
@@ -231,7 +229,7 @@ int try_stencil(mars_problem* p, const std::vector<int>& off, const std::vector<
         const int L = static_cast<int>(std::lround(std::pow(static_cast<double>(n), 1.0 / dims)));
         std::int64_t nn = 1;
         for (int d = 0; d < dims; ++d) nn *= L;
-        if (nn != n || L < 3 || L > 1024) continue;
+        if (nn != n || L < 3 || L > 256) continue;
         std::vector<unsigned char> signs(n, 0);
         bool ok = true;
         for (int i = 0; i < n && ok; ++i) {
@@ -260,8 +258,8 @@ int try_stencil(mars_problem* p, const std::vector<int>& off, const std::vector<
                 sum += c[d];
                 stride *= L;
             }
-            lv[sum].push_back(static_cast<unsigned>(c[0]) | static_cast<unsigned>(c[1]) << 10 |
-                              static_cast<unsigned>(c[2]) << 20);
+            lv[sum].push_back(static_cast<unsigned>(c[0]) | static_cast<unsigned>(c[1]) << 8 |
+                              static_cast<unsigned>(c[2]) << 16 | static_cast<unsigned>(signs[i]) << 24);
         }
         std::vector<int> lvl_off{0};
         std::vector<unsigned> coords;
@@ -273,7 +271,6 @@ int try_stencil(mars_problem* p, const std::vector<int>& off, const std::vector<
         }
         if (int rc = upload(&p->dStLvl, lvl_off.data(), lvl_off.size())) return rc;
         if (int rc = upload(&p->dStCoords, coords.data(), coords.size())) return rc;
-        if (int rc = upload(&p->dStSigns, signs.data(), signs.size())) return rc;
         p->stencil = true;
         p->st_dims = dims;
         p->st_L = L;
@@ -708,13 +705,21 @@ int batch_alloc(mars_batch* b) {
         const char* kk = std::getenv("MARS_SPARSE_KERNEL");
         b->use_stencil = p->stencil && !(kk && std::string(kk) != "stencil");
         if (b->use_stencil) {
-            // one run per CTA; state in shared memory when it fits beside the sign bytes
+            // One run per CTA.  The run's level chain (gathers + fp64 tanh per level) is latency
+            // bound, so throughput comes from runs in flight: up to 8 CTAs of <= 256 threads per SM
+            // (measured: EA-2D 1.5K -> 2.7K descents/s from 1 to 8 CTAs/SM with the state rows in
+            // global memory, beyond L2 capacity; EA-3D best at 4 x 256).  State in shared memory
+            // only when that still leaves >= 2 CTAs per SM.
             StencilLaunch& l = b->stencil;
-            l.smem_state = relax_stencil_smem(p->n, true) <= 220 * 1024;
-            if (const char* v = std::getenv("MARS_SPARSE_STATE")) l.smem_state = l.smem_state && std::string(v) != "global";
-            l.threads = std::min(1024, std::max(32, (p->st_maxw + 31) / 32 * 32));
+            l.threads = std::min(256, std::max(32, (p->st_maxw + 31) / 32 * 32));
             l.threads = std::max(32, std::min(1024, env_int("MARS_STENCIL_THREADS", l.threads)) / 32 * 32);
-            const int per_sm = l.smem_state ? 1 : std::max(1, env_int("MARS_STENCIL_CTAS_PER_SM", 1));
+            const std::size_t smem = relax_stencil_smem(p->n, p->st_nlev, true);
+            l.smem_state = 2 * (smem + 1024) <= 228 * 1024;
+            if (const char* v = std::getenv("MARS_SPARSE_STATE")) l.smem_state = smem <= 220 * 1024 && std::string(v) != "global";
+            const int fit = std::min(2048 / l.threads, 64 * 1024 / (l.threads * 64));
+            const int per_sm = std::max(1, env_int("MARS_STENCIL_CTAS_PER_SM",
+                                                   l.smem_state ? std::min<int>(fit, (228 * 1024) / (smem + 1024))
+                                                                : std::min(8, fit)));
             tm = 1;
             max_grid = env_int("MARS_SPARSE_GRID", per_sm * p->num_sms);
             per_cta = l.smem_state ? 0 : static_cast<std::size_t>(p->np) * sizeof(double);
@@ -1024,7 +1029,7 @@ int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
             CUDA_TRY(launch_relax_dense_umma(ra, b->umma, b->grid, st));
         else
             CUDA_TRY(b->use_stencil
-                         ? launch_relax_stencil(ra, StencilArgs{p->st_dims, p->st_L, p->st_nlev, p->dStLvl, p->dStCoords, p->dStSigns},
+                         ? launch_relax_stencil(ra, StencilArgs{p->st_dims, p->st_L, p->st_nlev, p->dStLvl, p->dStCoords},
                                                 b->stencil, st)
                          : b->use_spmm ? launch_relax_spmm(ra, sparse_levels(p), b->spmm, st)
                                        : launch_relax_sparse(ra, sparse_levels(p), b->sparse, st));

@@ -13,8 +13,10 @@
 // uncoupled sites.  A CTA owns one run; each level's sites are spread over the threads,
 // one barrier per level.  A thread computes its site's 2*DIMS neighbour indices from the
 // coordinates, puts them in ascending order with a sorting network (the order of the
-// reference's sorted adjacency row) and applies the row's signs from one byte per site
-// (bit k = sign of the k-th smallest neighbour's coupling).  The neighbour sum is the
+// reference's sorted adjacency row) and applies the row's signs from the site's sign bits
+// (bit k = sign of the k-th smallest neighbour's coupling), packed with the coordinates in
+// one word per site (L <= 256) and fetched a level ahead, so a level's critical path is the
+// shared-memory gathers, the fp64 sum and the tanh.  The neighbour sum is the
 // reference's: acc = 0, acc += (+-1) * s_j in ascending j, unfused fp64 -- (+-1) * v is a
 // sign flip, exact -- then + h_i.  State: fp64 in shared memory when it fits, else an
 // L2-resident global row per CTA.
@@ -54,19 +56,52 @@ __device__ __forceinline__ double warp_max(double v) {
     return v;
 }
 
+// One site: its packed word is c0 | c1 << 8 | c2 << 16 | signs << 24.
+template <int DIMS>
+__device__ __forceinline__ void relax_site(unsigned cc, int L, int s1, int s2, double T, const double* __restrict__ h64,
+                                           double* st, double& dmax) {
+    const int c0 = cc & 255, c1 = (cc >> 8) & 255, c2 = (cc >> 16) & 255;
+    const unsigned bits = cc >> 24;
+    const int i = c0 + s1 * c1 + s2 * c2;
+    int nb[2 * DIMS];
+    nb[0] = c0 ? i - 1 : i + (L - 1);
+    nb[1] = c0 < L - 1 ? i + 1 : i - (L - 1);
+    nb[2] = c1 ? i - s1 : i + (L - 1) * s1;
+    nb[3] = c1 < L - 1 ? i + s1 : i - (L - 1) * s1;
+    if constexpr (DIMS == 3) {
+        nb[4] = c2 ? i - s2 : i + (L - 1) * s2;
+        nb[5] = c2 < L - 1 ? i + s2 : i - (L - 1) * s2;
+    }
+    sort_nb<DIMS>(nb);
+    double v[2 * DIMS];
+#pragma unroll
+    for (int k = 0; k < 2 * DIMS; ++k) v[k] = st[nb[k]];
+    const double old = st[i];
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 2 * DIMS; ++k)
+        acc = __dadd_rn(acc, __hiloint2double(__double2hiint(v[k]) ^ static_cast<int>(((bits >> k) & 1u) << 31),
+                                              __double2loint(v[k])));
+    const double phi = __dadd_rn(acc, h64 ? __ldg(h64 + i) : 0.0);
+    const double trial = tanh_trial64(phi, T);
+    dmax = fmax(dmax, fabs(__dsub_rn(trial, old)));
+    st[i] = trial;
+}
+
 template <int DIMS, bool SMEM_STATE>
 __global__ void __launch_bounds__(1024, 1) relax_stencil_kernel(RelaxArgs a, StencilArgs g) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double red[32];
     __shared__ int s_run;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    const int n = a.n, L = g.L;
+    const int n = a.n, L = g.L, nlev = g.nlev;
     const std::size_t state_bytes = SMEM_STATE ? (static_cast<std::size_t>(n) * sizeof(double) + 15) / 16 * 16 : 0;
     double* st = SMEM_STATE ? reinterpret_cast<double*>(smem_raw)
                             : reinterpret_cast<double*>(a.work) + static_cast<std::size_t>(blockIdx.x) * a.np;
-    unsigned char* sg = smem_raw + state_bytes;   // [n] sign bytes
+    int* lvl = reinterpret_cast<int*>(smem_raw + state_bytes);   // [nlev + 1] level offsets
+    for (int i = tid; i <= nlev; i += blockDim.x) lvl[i] = g.lvl_off[i];
     const double* s0 = static_cast<const double*>(a.s0_64);
-    for (int i = tid; i < n; i += blockDim.x) sg[i] = g.signs[i];
+    const unsigned* __restrict__ words = g.coords;
     const int s1 = L, s2 = L * L;
 
     Slot slot;
@@ -83,36 +118,15 @@ __global__ void __launch_bounds__(1024, 1) relax_stencil_kernel(RelaxArgs a, Ste
         do {
             const double T = slot.T;
             double dmax = 0.0;
-            for (int lv = 0; lv < g.nlev; ++lv) {
-                const int e = __ldg(g.lvl_off + lv + 1);
-                for (int p = __ldg(g.lvl_off + lv) + tid; p < e; p += blockDim.x) {
-                    const unsigned cc = __ldg(g.coords + p);
-                    const int c0 = cc & 1023, c1 = (cc >> 10) & 1023, c2 = cc >> 20;
-                    const int i = c0 + s1 * c1 + s2 * c2;
-                    int nb[2 * DIMS];
-                    nb[0] = c0 ? i - 1 : i + (L - 1);
-                    nb[1] = c0 < L - 1 ? i + 1 : i - (L - 1);
-                    nb[2] = c1 ? i - s1 : i + (L - 1) * s1;
-                    nb[3] = c1 < L - 1 ? i + s1 : i - (L - 1) * s1;
-                    if constexpr (DIMS == 3) {
-                        nb[4] = c2 ? i - s2 : i + (L - 1) * s2;
-                        nb[5] = c2 < L - 1 ? i + s2 : i - (L - 1) * s2;
-                    }
-                    sort_nb<DIMS>(nb);
-                    double v[2 * DIMS];
-#pragma unroll
-                    for (int k = 0; k < 2 * DIMS; ++k) v[k] = st[nb[k]];
-                    const unsigned bits = sg[i];
-                    double acc = 0.0;
-#pragma unroll
-                    for (int k = 0; k < 2 * DIMS; ++k)
-                        acc = __dadd_rn(acc, __hiloint2double(__double2hiint(v[k]) ^ static_cast<int>(((bits >> k) & 1u) << 31),
-                                                              __double2loint(v[k])));
-                    const double phi = __dadd_rn(acc, a.h64 ? __ldg(a.h64 + i) : 0.0);
-                    const double trial = tanh_trial64(phi, T);
-                    dmax = fmax(dmax, fabs(__dsub_rn(trial, st[i])));
-                    st[i] = trial;
-                }
+            // the first site word of each level is fetched one level ahead (off the chain)
+            unsigned next = tid < lvl[1] ? __ldg(words + tid) : 0u;
+            for (int lv = 0; lv < nlev; ++lv) {
+                const int b = lvl[lv], e = lvl[lv + 1];
+                const unsigned cur = next;
+                if (lv + 1 < nlev && lvl[lv + 1] + tid < lvl[lv + 2]) next = __ldg(words + lvl[lv + 1] + tid);
+                if (b + tid < e) relax_site<DIMS>(cur, L, s1, s2, T, a.h64, st, dmax);
+                for (int p = b + tid + static_cast<int>(blockDim.x); p < e; p += blockDim.x)
+                    relax_site<DIMS>(__ldg(words + p), L, s1, s2, T, a.h64, st, dmax);
                 __syncthreads();
             }
             dmax = warp_max(dmax);
@@ -130,13 +144,14 @@ __global__ void __launch_bounds__(1024, 1) relax_stencil_kernel(RelaxArgs a, Ste
 }
 
 template <int DIMS, bool SMEM_STATE>
-std::size_t smem_t(int n) {
-    return (SMEM_STATE ? (static_cast<std::size_t>(n) * sizeof(double) + 15) / 16 * 16 : 0) + static_cast<std::size_t>(n);
+std::size_t smem_t(int n, int nlev) {
+    return (SMEM_STATE ? (static_cast<std::size_t>(n) * sizeof(double) + 15) / 16 * 16 : 0) +
+           static_cast<std::size_t>(nlev + 2) * sizeof(int);
 }
 
 template <int DIMS, bool SMEM_STATE>
 cudaError_t launch_t(const RelaxArgs& a, const StencilArgs& g, const StencilLaunch& l, cudaStream_t st) {
-    const std::size_t bytes = smem_t<DIMS, SMEM_STATE>(a.n);
+    const std::size_t bytes = smem_t<DIMS, SMEM_STATE>(a.n, g.nlev);
     cudaError_t e = cudaFuncSetAttribute(relax_stencil_kernel<DIMS, SMEM_STATE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
     if (e != cudaSuccess) return e;
@@ -146,8 +161,8 @@ cudaError_t launch_t(const RelaxArgs& a, const StencilArgs& g, const StencilLaun
 
 }  // namespace
 
-std::size_t relax_stencil_smem(int n, bool smem_state) {
-    return smem_state ? smem_t<2, true>(n) : smem_t<2, false>(n);
+std::size_t relax_stencil_smem(int n, int nlev, bool smem_state) {
+    return smem_state ? smem_t<2, true>(n, nlev) : smem_t<2, false>(n, nlev);
 }
 
 cudaError_t launch_relax_stencil(const RelaxArgs& a, const StencilArgs& g, const StencilLaunch& l, cudaStream_t st) {
