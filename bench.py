@@ -125,6 +125,33 @@ def cpu_reference_sample(w, runs: int, workers: int):
     return runs / dt, dt, b, kind
 
 
+def cpu_sweep_sample(w, workers: int, sweeps_each: int):
+    """Workloads whose descents are too long for a bounded CPU sample (cfg5: ~1e4 sweeps of a
+    16384^2 field each): the C port of the reference's mars_relax_sweep (solvers.cpp:150-161)
+    timed on `workers` host threads, `sweeps_each` sweeps of a random state at T = t_max / 2
+    each.  Returns (sweep-runs/s, seconds)."""
+    import threading
+    import numpy as np
+    from oracle.oracle import Oracle
+    from paper_1907_05124_b200.workloads import build_oracle_problem
+    orc = Oracle("port")
+    p = build_oracle_problem(orc, w)
+    states = [np.random.default_rng(k).uniform(-1, 1, w.n) for k in range(workers)]
+
+    def work(st):
+        for _ in range(sweeps_each):
+            p.relax_sweep(st, 0.5 * w.t_max)
+
+    th = [threading.Thread(target=work, args=(st,)) for st in states]
+    t0 = time.perf_counter()
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    dt = time.perf_counter() - t0
+    return workers * sweeps_each / dt, dt
+
+
 def default_cpu_runs(w, cores):
     # bounded sample (~10-30 s of host work): one descent per host thread for dense N=2000,
     # more for the cheaper instances
@@ -266,6 +293,16 @@ def run_b200(args, w, rank, world, local_rank, dist):
     if not args.no_cpu and world == 1:
         cores = os.cpu_count() or 1
         cruns = args.cpu_runs or default_cpu_runs(w, cores)
+        if w.name == "cfg5_sk16384" and not args.cpu_runs:
+            each = 4
+            srs, dt = cpu_sweep_sample(w, cores, each)
+            mean_sweeps = sweeps / max(1, int((rec.status != 1).sum()))
+            cpu = {"value": srs / mean_sweeps, "unit": "descents/s", "cores": cores, "kind": "port",
+                   "sample": f"C port of mars_relax_sweep, {each} sweeps on each of {cores} host threads "
+                             f"({dt:.1f} s); descents/s = sweep-runs/s / {mean_sweeps:.0f} (mean sweeps "
+                             f"per descent of this workload, measured above)",
+                   "sweep_runs_per_s": srs}
+            cruns = 0
         if cruns > 0:
             v, dt, b, kind = cpu_reference_sample(w, cruns, cores)
             cpu = {"value": v, "unit": "descents/s", "cores": cores, "kind": kind,
