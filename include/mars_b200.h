@@ -117,6 +117,17 @@ int mars_problem_from_edges(int32_t n, int64_t m, const int32_t* u, const int32_
 void mars_problem_destroy(mars_problem_t* p);
 int mars_problem_info(const mars_problem_t* p, mars_problem_info_t* out);
 
+/* problem_hash (io.hpp, io.cpp:260-290): FNV-1a over n, the stored upper-triangle couplings in
+ * visit_upper order and the nonzero field entries.  mars_instance_hash hashes an instance
+ * given as dense J (J != NULL) or an edge list, with the same validation and storage rule as
+ * the constructors, without touching a device. */
+int mars_problem_hash(const mars_problem_t* p, uint64_t* out);
+int mars_instance_hash(int32_t n, const double* J, int64_t m, const int32_t* u, const int32_t* v,
+                       const double* w, const double* h, uint64_t* out);
+
+/* All n rows of IsingProblem::row_values (model.cpp:173-182) into out[n*n] (write_matrix). */
+int mars_problem_rows(const mars_problem_t* p, double* out);
+
 /* energy / cut_value of one spin vector, on the device, exact reference order
  * (model.cpp:203-229). */
 int mars_energy(const mars_problem_t* p, const int8_t* spins, double* energy, double* cut);

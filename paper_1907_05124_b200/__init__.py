@@ -12,3 +12,4 @@ from .mars import (  # noqa: F401
     mars_run_plan, mars_sweep, round_spins, run_batch, run_batch_with, run_shard, shard_range,
     splitmix64, sub_seed, validate,
 )
+from . import io  # noqa: F401,E402  (instance I/O and result documents, io.hpp mirror)

@@ -66,6 +66,9 @@ SIGNATURES = {
     "mars_problem_from_edges": (C.c_int, [i32, i64, vp, vp, vp, vp, i32, i32, C.POINTER(vp)]),
     "mars_problem_destroy": (None, [vp]),
     "mars_problem_info": (C.c_int, [vp, C.POINTER(mars_problem_info_t)]),
+    "mars_problem_hash": (C.c_int, [vp, vp]),
+    "mars_instance_hash": (C.c_int, [i32, vp, i64, vp, vp, vp, vp, vp]),
+    "mars_problem_rows": (C.c_int, [vp, vp]),
     "mars_energy": (C.c_int, [vp, vp, vp, vp]),
     "mars_validate_params": (C.c_int, [P_params]),
     "mars_run_count": (C.c_int, [P_params, i64, vp]),

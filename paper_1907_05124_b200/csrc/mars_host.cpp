@@ -808,8 +808,12 @@ int mars_initial_state(uint64_t seed, int32_t n, double* s) {
     return MARS_OK;
 }
 
-int mars_problem_dense(int32_t n, const double* J, const double* h, int32_t device,
-                       int32_t kernel, mars_problem_t** out) {
+}  // extern "C"
+
+namespace {
+
+// Host side of IsingProblem::dense (model.cpp:47-72): validation and the stored copy.
+int host_dense(int32_t n, const double* J, const double* h, mars_problem** out) {
     if (n <= 0) return fail(MARS_ERR_INPUT, "problem size must be positive");
     if (!J || !out) return fail(MARS_ERR_INPUT, "null argument");
     for (int i = 0; i < n; ++i) {                                          // model.cpp:55-64
@@ -826,12 +830,14 @@ int mars_problem_dense(int32_t n, const double* J, const double* h, int32_t devi
     p->J.assign(J, J + static_cast<std::size_t>(n) * n);
     p->h.assign(n, 0.0);
     if (h) std::copy(h, h + n, p->h.begin());
-    return finish_problem(p, device, kernel, out);
+    *out = p;
+    return MARS_OK;
 }
 
-int mars_problem_from_edges(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
-                            const double* w, const double* h, int32_t device, int32_t kernel,
-                            mars_problem_t** out) {
+// Host side of IsingProblem::from_edges (model.cpp:74-131): validation, the 5% storage rule,
+// dense accumulation or the canonical (sorted) adjacency.
+int host_edges(int32_t n, int64_t m, const int32_t* u, const int32_t* v, const double* w, const double* h,
+               mars_problem** out) {
     if (n <= 0) return fail(MARS_ERR_INPUT, "problem size must be positive");
     if (!out || (m > 0 && (!u || !v || !w))) return fail(MARS_ERR_INPUT, "null argument");
     for (std::int64_t k = 0; k < m; ++k) {                                  // model.cpp:80-84
@@ -881,7 +887,100 @@ int mars_problem_from_edges(int32_t n, int64_t m, const int32_t* u, const int32_
             }
         }
     }
+    *out = p;
+    return MARS_OK;
+}
+
+// problem_hash (io.cpp:260-290): FNV-1a over n, the stored upper-triangle couplings in
+// visit_upper order (model.cpp:184-196) and the nonzero field entries, little-endian bytes.
+std::uint64_t hash_of(const mars_problem* p) {
+    std::uint64_t hv = 0xcbf29ce484222325ull;
+    auto mix64 = [&hv](std::uint64_t x) {
+        for (int b = 0; b < 8; ++b) {
+            hv ^= (x >> (8 * b)) & 0xffu;
+            hv *= 0x100000001b3ull;
+        }
+    };
+    auto mix_double = [&](double d) {
+        std::uint64_t bits;
+        std::memcpy(&bits, &d, sizeof bits);
+        mix64(bits);
+    };
+    const int n = p->n;
+    mix64(static_cast<std::uint64_t>(n));
+    for (int i = 0; i < n; ++i) {
+        if (p->dense) {
+            for (int k = i + 1; k < n; ++k) {
+                const double w = p->J[static_cast<std::size_t>(i) * n + k];
+                if (w != 0.0) {
+                    mix64(static_cast<std::uint64_t>(i));
+                    mix64(static_cast<std::uint64_t>(k));
+                    mix_double(w);
+                }
+            }
+        } else {
+            for (int e = p->off[i]; e < p->off[i + 1]; ++e)
+                if (p->idx[e] > i) {
+                    mix64(static_cast<std::uint64_t>(i));
+                    mix64(static_cast<std::uint64_t>(p->idx[e]));
+                    mix_double(p->wt[e]);
+                }
+        }
+    }
+    for (int i = 0; i < n; ++i)
+        if (p->h[i] != 0.0) {
+            mix64(static_cast<std::uint64_t>(i));
+            mix_double(p->h[i]);
+        }
+    return hv;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mars_problem_dense(int32_t n, const double* J, const double* h, int32_t device,
+                       int32_t kernel, mars_problem_t** out) {
+    mars_problem* p = nullptr;
+    if (int rc = host_dense(n, J, h, &p)) return rc;
     return finish_problem(p, device, kernel, out);
+}
+
+int mars_problem_from_edges(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                            const double* w, const double* h, int32_t device, int32_t kernel,
+                            mars_problem_t** out) {
+    mars_problem* p = nullptr;
+    if (int rc = host_edges(n, m, u, v, w, h, &p)) return rc;
+    return finish_problem(p, device, kernel, out);
+}
+
+int mars_problem_hash(const mars_problem_t* p, uint64_t* out) {
+    if (!p || !out) return fail(MARS_ERR_INPUT, "null argument");
+    *out = hash_of(p);
+    return MARS_OK;
+}
+
+int mars_instance_hash(int32_t n, const double* J, int64_t m, const int32_t* u, const int32_t* v,
+                       const double* w, const double* h, uint64_t* out) {
+    if (!out) return fail(MARS_ERR_INPUT, "null argument");
+    mars_problem* p = nullptr;
+    if (int rc = J ? host_dense(n, J, h, &p) : host_edges(n, m, u, v, w, h, &p)) return rc;
+    *out = hash_of(p);
+    delete p;
+    return MARS_OK;
+}
+
+int mars_problem_rows(const mars_problem_t* p, double* out) {
+    if (!p || !out) return fail(MARS_ERR_INPUT, "null argument");
+    const int n = p->n;
+    if (p->dense) {
+        std::copy(p->J.begin(), p->J.end(), out);
+    } else {                                                                // row_values, model.cpp:173-182
+        std::fill(out, out + static_cast<std::size_t>(n) * n, 0.0);
+        for (int i = 0; i < n; ++i)
+            for (int e = p->off[i]; e < p->off[i + 1]; ++e) out[static_cast<std::size_t>(i) * n + p->idx[e]] = p->wt[e];
+    }
+    return MARS_OK;
 }
 
 void mars_problem_destroy(mars_problem_t* p) { delete p; }

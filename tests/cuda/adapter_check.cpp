@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdio>
 
+#include "mars/io.hpp"
 #include "mars/rng.hpp"
 #include "mars/runner.hpp"
 #include "mars_gpu_adapter.hpp"
@@ -43,6 +44,16 @@ int main() {
             }
         }
         const double frac = total ? static_cast<double>(same) / total : 1.0;
+        // the reference's own result document (io.cpp:480-538) over the
+        // GPU batch; identical to the reference's document whenever every run matches
+        const std::string dref = result_document_to_string(make_result_document(name, p, mp, ref, DocDetail::Full, false));
+        const std::string dgpu = result_document_to_string(make_result_document(name, p, mp, gpu, DocDetail::Full, false));
+        int iters_same = 0;
+        for (size_t k = 0; k < ref.runs.size(); ++k) iters_same += ref.runs[k].descent_iters == gpu.runs[k].descent_iters;
+        const bool all_same = same == total && iters_same == static_cast<int>(ref.runs.size());
+        if (all_same && dref != dgpu) ++failures;
+        std::printf("    result document: %s (%zu bytes; iters identical %d/%zu)\n",
+                    dref == dgpu ? "byte-identical" : "differs", dref.size(), iters_same, ref.runs.size());
         const bool ok = frac >= min_same && gpu.runs.size() == ref.runs.size() &&
                         gpu.skipped_runs == ref.skipped_runs &&
                         std::abs(gpu.best_energy - ref.best_energy) <= 1e-6 * std::abs(ref.best_energy) + 1e-9;

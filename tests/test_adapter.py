@@ -10,14 +10,16 @@ import pytest
 from conftest import ROOT, gpu_available
 
 REF = "/root/reference/proj"
+# nlohmann/json for the reference's io.cpp (result documents); vendored in the image
+JSON_DIR = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
 BIN = os.path.join(ROOT, "tests", "cuda", "adapter_check")
 
 
 def build_adapter_check():
     lib_dir = os.path.join(ROOT, "paper_1907_05124_b200")
-    cmd = ["g++", "-std=c++20", "-O2", f"-I{REF}/include", f"-I{ROOT}/include",
+    cmd = ["g++", "-std=c++20", "-O2", f"-I{REF}/include", f"-I{ROOT}/include", f"-I{JSON_DIR}",
            f"-I{ROOT}/tests/cuda", os.path.join(ROOT, "tests", "cuda", "adapter_check.cpp"),
-           f"{REF}/src/model.cpp", f"{REF}/src/solvers.cpp", f"{REF}/src/runner.cpp",
+           f"{REF}/src/model.cpp", f"{REF}/src/solvers.cpp", f"{REF}/src/runner.cpp", f"{REF}/src/io.cpp",
            f"-L{lib_dir}", "-lmars_b200", f"-Wl,-rpath,{lib_dir}", "-Wl,-rpath,$ORIGIN/../../paper_1907_05124_b200",
            "-lpthread", "-o", BIN]
     subprocess.run(cmd, check=True, capture_output=True, text=True)
