@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
+#include "ref_tanh.cuh"
 #include "slot.cuh"
 #include "umma.cuh"
 
@@ -35,10 +36,8 @@ namespace {
 constexpr int kMaxConsumerWarps = 16;
 constexpr int kMaxSlots = 16;   // chunks in flight
 
-__device__ __forceinline__ double tanh_trial64(double phi, double t) {
-    if (t < kTempFloor) return phi > 0.0 ? -1.0 : (phi < 0.0 ? 1.0 : 0.0);
-    return -tanh(__ddiv_rn(phi, t));
-}
+// tanh_trial (solvers.cpp:145-148) with the reference's own tanh, bit for bit (ref_tanh.cuh)
+__device__ __forceinline__ double tanh_trial64(double phi, double t) { return ref_tanh_trial(phi, t); }
 
 // Row e of a state array, with the coupling sign (bit 31 of the code) applied: (+-1) * v.
 // The byte offset e << 3 drops the sign bit, so the address needs no mask.

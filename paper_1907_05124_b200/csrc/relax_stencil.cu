@@ -23,15 +23,14 @@
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
+#include "ref_tanh.cuh"
 #include "slot.cuh"
 
 namespace marsb200 {
 namespace {
 
-__device__ __forceinline__ double tanh_trial64(double phi, double t) {
-    if (t < kTempFloor) return phi > 0.0 ? -1.0 : (phi < 0.0 ? 1.0 : 0.0);
-    return -tanh(__ddiv_rn(phi, t));
-}
+// tanh_trial (solvers.cpp:145-148) with the reference's own tanh, bit for bit (ref_tanh.cuh)
+__device__ __forceinline__ double tanh_trial64(double phi, double t) { return ref_tanh_trial(phi, t); }
 
 __device__ __forceinline__ void cswap(int& a, int& b) {
     const int lo = min(a, b), hi = max(a, b);

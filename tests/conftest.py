@@ -33,6 +33,13 @@ def _ensure_built():
     probe = os.path.join(ROOT, "tests", "cuda", "libumma_probe.so")
     if not os.path.exists(probe):
         build_probe()
+    tp = os.path.join(ROOT, "tests", "cuda", "libtanh_probe.so")
+    srcs = [os.path.join(ROOT, "tests", "cuda", "tanh_probe.cu"),
+            os.path.join(ROOT, "paper_1907_05124_b200", "csrc", "ref_tanh.cuh")]
+    if not os.path.exists(tp) or os.path.getmtime(tp) < max(os.path.getmtime(x) for x in srcs):
+        subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2", "-std=c++17",
+                        "-Xcompiler", "-fPIC", "-shared", "-o", tp, srcs[0]], check=True,
+                       capture_output=True)
 
 
 def build_probe():
