@@ -58,3 +58,36 @@ static double g_tanh(double x){
   } else z=1.0-1e-300;
   return (int32_t)jx>=0 ? z : -z;
 }
+
+/* Branch-free form of g_tanh for the device: the same operations, every reconstruction
+ * computed and selected (lanes of a warp take different expm1 branches otherwise). */
+static double g_tanh_bf(double x){
+  const double invln2=1.4426950408889634, ln2_hi=0.6931471803691238, ln2_lo=1.9082149292705877e-10;
+  const double Q1=-0.03333333333333313, Q2=0.0015873015872548146, Q3=-7.93650757867488e-05,
+               Q4=4.008217827329362e-06, Q5=-2.0109921818362437e-07;
+  uint64_t b=g_bits(x); uint32_t ix=(uint32_t)(b>>32)&0x7fffffffu;
+  double ax=fabs(x); int small = ix<=0x3fefffffu;                   /* |x| < 1 */
+  double a = small ? ax*-2.0 : ax+ax;                               /* expm1 argument */
+  uint32_t ha=(uint32_t)(g_bits(a)>>32)&0x7fffffffu;
+  int k = ha<=0x3fd62e42u ? 0 : (int32_t)((a<0?-0.5:0.5)+a*invln2);
+  double tk=(double)k, hi=fma(-tk,ln2_hi,a), lo=tk*ln2_lo, xr=hi-lo, c=(hi-xr)-lo;
+  double hfx=xr*0.5, hxs=xr*hfx;
+  double R2=fma(hxs,Q3,Q2), R3=fma(hxs,Q5,Q4), h2=hxs*hxs, R1=fma(hxs,Q1,1.0), h4=h2*h2;
+  double r1=fma(h4,R3,fma(h2,R2,R1)), t=fma(-r1,hfx,3.0);
+  double e=((r1-t)/fma(-xr,t,6.0))*hxs;
+  double r0=xr-fma(e,xr,-hxs);
+  double e2=fma(e-c,xr,-c)-hxs;
+  double rm1=fma(xr-e2,0.5,-0.5);
+  double rp1= xr<-0.25 ? (e2-(xr+0.5))*-2.0 : fma(xr-e2,2.0,1.0);
+  double rbig=g_add_hi(1.0-(e2-xr),k)-1.0;
+  int kl = k<0?0:(k>19?19:k);
+  double rmid=g_add_hi(g_dbl((uint64_t)(0x3ff00000u-(0x200000u>>kl))<<32)-(e2-xr),k);
+  int kh = k<20?20:(k>1023?1023:k);
+  double rhi=g_add_hi((xr-(e2+g_dbl((uint64_t)((uint32_t)(0x3ff-kh)<<20)<<32)))+1.0,k);
+  double em1 = k==0 ? r0 : k==-1 ? rm1 : k==1 ? rp1 : ((uint32_t)(k+1)>57u ? rbig : (k<20 ? rmid : rhi));
+  double q=(small ? -em1 : 2.0)/(em1+2.0);
+  double z = small ? q : 1.0-q;
+  if(ix>0x4035ffffu) z=1.0;                                          /* |x| >= 22 */
+  if(ix<=0x3c7fffffu) return (ix|(uint32_t)b)==0 ? x : (1.0+x)*x;    /* |x| < 2^-55, +-0 */
+  return (int64_t)b>=0 ? z : -z;
+}
