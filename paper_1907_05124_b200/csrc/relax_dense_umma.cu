@@ -38,6 +38,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <utility>
 
 #include "kernels.cuh"
@@ -111,6 +112,7 @@ struct UmmaParams {
     __half* s_hi_w;
     __half* s_lo_w;
     int nb;                  // blocks per sweep = np / TB
+    int l2hint;              // coupling tiles loaded with an L2 evict_last hint (shared by all CTAs)
 };
 
 __device__ __forceinline__ void split16(float v, __half& hi, __half& lo, float& back) {
@@ -307,6 +309,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
             tma_prefetch_desc(&tm_slo);
             tma_prefetch_desc(&tm_jhi);
             if (JLO) tma_prefetch_desc(&tm_jlo);
+            const std::uint64_t jpol = policy_evict_last();
             std::uint32_t g = 0, it = 0;
             long long w_ready = 0, w_empty = 0;
             for (;;) {
@@ -338,8 +341,15 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         mbar_arrive_expect_tx(&ctl.full[s], JLO ? STAGE_BYTES : STAGE_BYTES - TILE_J);
                         tma_load_2d(st, &tm_shi, &ctl.full[s], c * KC, row0);
                         tma_load_2d(st + TILE_A, &tm_slo, &ctl.full[s], c * KC, row0);
-                        tma_load_2d(st + 2 * TILE_A, &tm_jhi, &ctl.full[s], c * KC, b * TB);
-                        if (JLO) tma_load_2d(st + 2 * TILE_A + TILE_J, &tm_jlo, &ctl.full[s], c * KC, b * TB);
+                        // the coupling tiles are read by every CTA every sweep: keep them in L2
+                        // ahead of the per-CTA state planes (155 MB at 148 CTAs > L2)
+                        if (up.l2hint) {
+                            tma_load_2d_hint(st + 2 * TILE_A, &tm_jhi, &ctl.full[s], c * KC, b * TB, jpol);
+                            if (JLO) tma_load_2d_hint(st + 2 * TILE_A + TILE_J, &tm_jlo, &ctl.full[s], c * KC, b * TB, jpol);
+                        } else {
+                            tma_load_2d(st + 2 * TILE_A, &tm_jhi, &ctl.full[s], c * KC, b * TB);
+                            if (JLO) tma_load_2d(st + 2 * TILE_A + TILE_J, &tm_jlo, &ctl.full[s], c * KC, b * TB);
+                        }
                     }
                 }
             }
@@ -635,7 +645,8 @@ int relax_dense_umma_block() { return TB; }
 std::size_t relax_dense_umma_plane_rows(int grid) { return static_cast<std::size_t>(grid) * TM; }
 
 cudaError_t launch_relax_dense_umma(const RelaxArgs& a, const UmmaLaunch& u, int grid, cudaStream_t st) {
-    UmmaParams up{u.s_hi, u.s_hi, u.s_lo, a.np / TB};
+    const char* hint = std::getenv("MARS_UMMA_L2HINT");
+    UmmaParams up{u.s_hi, u.s_hi, u.s_lo, a.np / TB, hint ? std::atoi(hint) : 1};
     if (a.np % TB != 0) return cudaErrorInvalidValue;
     cudaError_t e;
     if (u.jlo) {

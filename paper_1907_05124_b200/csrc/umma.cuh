@@ -64,7 +64,7 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t pari
         if ((spin & 1023u) == 0) {
             std::uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            if (t - t0 > 20000000000ull) __trap();
+            if (t - t0 > 120000000000ull) __trap();   // 120 s: hang detector (profiler replays are slow)
         }
     }
 }
@@ -83,6 +83,29 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, st
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
         "[%0], [%1, {%3, %4}], [%2];\n" ::"r"(smem_u32(smem_dst)),
         "l"(reinterpret_cast<std::uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+// L2 eviction-priority policies for the TMA loads (createpolicy): operands re-read by every
+// CTA (the coupling tiles) stay in L2 ahead of per-CTA streams.
+__device__ __forceinline__ std::uint64_t policy_evict_last() {
+    std::uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ std::uint64_t policy_evict_first() {
+    std::uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
+}
+
+// tma_load_2d with an L2 cache-eviction hint.
+__device__ __forceinline__ void tma_load_2d_hint(void* smem_dst, const void* tmap, std::uint64_t* bar,
+                                                 int c0, int c1, std::uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%3, %4}], [%2], %5;\n" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<std::uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
         : "memory");
 }
 

@@ -330,8 +330,9 @@ def test_device_tanh_matches_libm():
     assert np.array_equal(e[fin].view(np.int64), want_e[fin].view(np.int64))
 
 
-@pytest.mark.parametrize("kind", ["er_pm1", "er_gauss_field", "ea2d", "ea3d", "er_dense_storage"])
-def test_sparse_kernels_exact_vs_reference(kind, port):
+@pytest.mark.parametrize("kind", ["er_pm1", "er_gauss_field", "ea2d", "ea3d", "er_dense_storage",
+                                  "ea2d_site_pairs"])
+def test_sparse_kernels_exact_vs_reference(kind, port, monkeypatch):
     """With the reference's own tanh on the device, the fp64 sparse kernels reproduce the
     reference's descents exactly: every status, iteration count, energy, cut and spin."""
     from oracle.oracle import params
@@ -350,6 +351,9 @@ def test_sparse_kernels_exact_vs_reference(kind, port):
         n, (u, v, w) = 24 * 24, mb.gen_ea(24, 2, 3)
     elif kind == "ea3d":
         n, (u, v, w) = 8 ** 3, mb.gen_ea(8, 3, 4)
+    elif kind == "ea2d_site_pairs":   # levels wider than the CTA: two sites per thread
+        n, (u, v, w) = 48 * 48, mb.gen_ea(48, 2, 6)
+        monkeypatch.setenv("MARS_STENCIL_THREADS", "32")
     else:   # 6% graph stored dense by the reference, relaxed by the sparse path
         n, (u, v, w) = 200, mb.gen_er(200, 0.06, 9)
     p = mb.IsingProblem.from_edges(n, (u, v, w), h)
