@@ -87,51 +87,6 @@ __device__ __forceinline__ void relax_site(unsigned cc, int L, int s1, int s2, d
     st[i] = trial;
 }
 
-// Two sites of one level (never coupled, so no store of one can feed the other's gathers):
-// all gathers first, then both exact-order sums and tanh chains interleaved, then the stores.
-template <int DIMS>
-__device__ __forceinline__ void relax_site_pair(unsigned cc0, unsigned cc1, int L, int s1, int s2, double T,
-                                                const double* __restrict__ h64, double* st, double& dmax) {
-    const unsigned cc[2] = {cc0, cc1};
-    int i[2];
-    double v[2][2 * DIMS], old[2], acc[2];
-#pragma unroll
-    for (int m = 0; m < 2; ++m) {
-        const int c0 = cc[m] & 255, c1 = (cc[m] >> 8) & 255, c2 = (cc[m] >> 16) & 255;
-        i[m] = c0 + s1 * c1 + s2 * c2;
-        int nb[2 * DIMS];
-        nb[0] = c0 ? i[m] - 1 : i[m] + (L - 1);
-        nb[1] = c0 < L - 1 ? i[m] + 1 : i[m] - (L - 1);
-        nb[2] = c1 ? i[m] - s1 : i[m] + (L - 1) * s1;
-        nb[3] = c1 < L - 1 ? i[m] + s1 : i[m] - (L - 1) * s1;
-        if constexpr (DIMS == 3) {
-            nb[4] = c2 ? i[m] - s2 : i[m] + (L - 1) * s2;
-            nb[5] = c2 < L - 1 ? i[m] + s2 : i[m] - (L - 1) * s2;
-        }
-        sort_nb<DIMS>(nb);
-#pragma unroll
-        for (int k = 0; k < 2 * DIMS; ++k) v[m][k] = st[nb[k]];
-        old[m] = st[i[m]];
-    }
-#pragma unroll
-    for (int m = 0; m < 2; ++m) {
-        const unsigned bits = cc[m] >> 24;
-        acc[m] = 0.0;
-#pragma unroll
-        for (int k = 0; k < 2 * DIMS; ++k)
-            acc[m] = __dadd_rn(acc[m], __hiloint2double(__double2hiint(v[m][k]) ^ static_cast<int>(((bits >> k) & 1u) << 31),
-                                                        __double2loint(v[m][k])));
-    }
-    double trial[2];
-#pragma unroll
-    for (int m = 0; m < 2; ++m) {
-        trial[m] = tanh_trial64(__dadd_rn(acc[m], h64 ? __ldg(h64 + i[m]) : 0.0), T);
-        dmax = fmax(dmax, fabs(__dsub_rn(trial[m], old[m])));
-    }
-    st[i[0]] = trial[0];
-    st[i[1]] = trial[1];
-}
-
 template <int DIMS, bool SMEM_STATE>
 __global__ void __launch_bounds__(1024, 1) relax_stencil_kernel(RelaxArgs a, StencilArgs g) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -168,13 +123,8 @@ __global__ void __launch_bounds__(1024, 1) relax_stencil_kernel(RelaxArgs a, Ste
                 const int b = lvl[lv], e = lvl[lv + 1];
                 const unsigned cur = next;
                 if (lv + 1 < nlev && lvl[lv + 1] + tid < lvl[lv + 2]) next = __ldg(words + lvl[lv + 1] + tid);
-                const int p2 = b + tid + static_cast<int>(blockDim.x);
-                if (p2 < e) {
-                    relax_site_pair<DIMS>(cur, __ldg(words + p2), L, s1, s2, T, a.h64, st, dmax);
-                } else if (b + tid < e) {
-                    relax_site<DIMS>(cur, L, s1, s2, T, a.h64, st, dmax);
-                }
-                for (int p = p2 + static_cast<int>(blockDim.x); p < e; p += blockDim.x)
+                if (b + tid < e) relax_site<DIMS>(cur, L, s1, s2, T, a.h64, st, dmax);
+                for (int p = b + tid + static_cast<int>(blockDim.x); p < e; p += blockDim.x)
                     relax_site<DIMS>(__ldg(words + p), L, s1, s2, T, a.h64, st, dmax);
                 __syncthreads();
             }

@@ -331,7 +331,7 @@ def test_device_tanh_matches_libm():
 
 
 @pytest.mark.parametrize("kind", ["er_pm1", "er_gauss_field", "ea2d", "ea3d", "er_dense_storage",
-                                  "ea2d_site_pairs"])
+                                  "ea2d_narrow_ctas"])
 def test_sparse_kernels_exact_vs_reference(kind, port, monkeypatch):
     """With the reference's own tanh on the device, the fp64 sparse kernels reproduce the
     reference's descents exactly: every status, iteration count, energy, cut and spin."""
@@ -351,7 +351,7 @@ def test_sparse_kernels_exact_vs_reference(kind, port, monkeypatch):
         n, (u, v, w) = 24 * 24, mb.gen_ea(24, 2, 3)
     elif kind == "ea3d":
         n, (u, v, w) = 8 ** 3, mb.gen_ea(8, 3, 4)
-    elif kind == "ea2d_site_pairs":   # levels wider than the CTA: two sites per thread
+    elif kind == "ea2d_narrow_ctas":   # levels wider than the CTA: several sites per thread
         n, (u, v, w) = 48 * 48, mb.gen_ea(48, 2, 6)
         monkeypatch.setenv("MARS_STENCIL_THREADS", "32")
     else:   # 6% graph stored dense by the reference, relaxed by the sparse path
