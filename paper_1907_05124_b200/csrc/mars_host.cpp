@@ -145,8 +145,45 @@ struct mars_problem {
     __half* dJlo = nullptr;
     bool jlo = true;                // J_lo nonzero somewhere (non-integer couplings)
     CUtensorMap tm_jhi{}, tm_jlo{};
+    // Buffer pool for the batches run on this problem: repeated run_batch calls reuse their
+    // pinned host and device allocations (a 65536 x 2000 fp64 plan is 1 GB pinned) instead of
+    // allocating and freeing them every call.
+    struct PoolBuf {
+        void* ptr;
+        std::size_t bytes;
+        bool pinned;
+    };
+    std::vector<PoolBuf> pool;
+
+    void* take(std::size_t bytes, bool pinned) {
+        bytes = std::max<std::size_t>(bytes, 16);
+        for (std::size_t k = 0; k < pool.size(); ++k)
+            if (pool[k].pinned == pinned && pool[k].bytes >= bytes && pool[k].bytes <= 2 * bytes + 4096) {
+                void* ptr = pool[k].ptr;
+                pool.erase(pool.begin() + static_cast<std::ptrdiff_t>(k));
+                return ptr;
+            }
+        void* ptr = nullptr;
+        if ((pinned ? cudaMallocHost(&ptr, bytes) : cudaMalloc(&ptr, bytes)) != cudaSuccess) return nullptr;
+        sizes.emplace_back(ptr, bytes);
+        return ptr;
+    }
+    void give(void* ptr, bool pinned) {
+        if (!ptr) return;
+        for (const auto& sz : sizes)
+            if (sz.first == ptr) {
+                pool.push_back({ptr, sz.second, pinned});
+                return;
+            }
+    }
+    std::vector<std::pair<void*, std::size_t>> sizes;   // every block this pool allocated
 
     ~mars_problem() {
+        cudaSetDevice(device);
+        for (const auto& b : pool) {
+            if (b.pinned) cudaFreeHost(b.ptr);
+            else cudaFree(b.ptr);
+        }
         cudaFree(dJhi);
         cudaFree(dJlo);
         cudaSetDevice(device);
@@ -531,24 +568,16 @@ struct mars_batch {
     ~mars_batch() {
         if (!p) return;
         cudaSetDevice(p->device);
-        cudaFreeHost(h_s0);
-        cudaFreeHost(h_order);
-        cudaFreeHost(h_temp);
-        cudaFreeHost(h_status);
-        cudaFree(d_s0);
-        cudaFree(d_temp);
-        cudaFree(d_order);
-        cudaFree(d_work);
-        cudaFree(d_queue);
-        cudaFree(d_status);
-        cudaFree(d_iters);
-        cudaFree(d_elapsed);
-        cudaFree(d_spins);
-        cudaFree(d_energy);
-        cudaFree(d_cut);
-        cudaFree(d_part_e);
-        cudaFree(d_part_i);
-        cudaFree(d_best);
+        cudaStreamSynchronize(p->stream);
+        for (void* h : {static_cast<void*>(h_s0), static_cast<void*>(h_order), static_cast<void*>(h_temp),
+                        static_cast<void*>(h_status)})
+            p->give(h, true);
+        for (void* d : {d_s0, static_cast<void*>(d_temp), static_cast<void*>(d_order), d_work,
+                        static_cast<void*>(d_queue), static_cast<void*>(d_status), static_cast<void*>(d_iters),
+                        static_cast<void*>(d_elapsed), static_cast<void*>(d_spins), static_cast<void*>(d_energy),
+                        static_cast<void*>(d_cut), static_cast<void*>(d_part_e), static_cast<void*>(d_part_i),
+                        static_cast<void*>(d_best)})
+            p->give(d, false);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
     }
@@ -649,25 +678,42 @@ int batch_alloc(mars_batch* b) {
     const std::size_t n = static_cast<std::size_t>(p->n);
     CUDA_TRY(cudaSetDevice(p->device));
     b->s0_elem = p->kernel == MARS_KERNEL_CSR ? sizeof(double) : sizeof(float);
-    CUDA_TRY(cudaMallocHost(&b->h_s0, cnt * n * b->s0_elem));
-    CUDA_TRY(cudaMallocHost(&b->h_order, cnt * sizeof(int)));
-    CUDA_TRY(cudaMallocHost(&b->h_temp, cnt * sizeof(double)));
-    CUDA_TRY(cudaMallocHost(&b->h_status, cnt));
-    CUDA_TRY(cudaMalloc(&b->d_s0, cnt * n * b->s0_elem));
-    CUDA_TRY(cudaMalloc(&b->d_temp, cnt * sizeof(double)));
-    CUDA_TRY(cudaMalloc(&b->d_order, cnt * sizeof(int)));
-    CUDA_TRY(cudaMalloc(&b->d_queue, sizeof(int)));
-    CUDA_TRY(cudaMalloc(&b->d_status, cnt));
-    CUDA_TRY(cudaMalloc(&b->d_iters, cnt * sizeof(long long)));
-    CUDA_TRY(cudaMalloc(&b->d_elapsed, cnt * sizeof(double)));
-    CUDA_TRY(cudaMalloc(&b->d_spins, cnt * n));
-    CUDA_TRY(cudaMalloc(&b->d_energy, cnt * sizeof(double)));
-    CUDA_TRY(cudaMalloc(&b->d_cut, cnt * sizeof(double)));
+    if (!(b->h_s0 = static_cast<decltype(b->h_s0)>(p->take(cnt * n * b->s0_elem, true))))
+        return fail(MARS_ERR_CUDA, "pinned host allocation failed");
+    if (!(b->h_order = static_cast<decltype(b->h_order)>(p->take(cnt * sizeof(int), true))))
+        return fail(MARS_ERR_CUDA, "pinned host allocation failed");
+    if (!(b->h_temp = static_cast<decltype(b->h_temp)>(p->take(cnt * sizeof(double), true))))
+        return fail(MARS_ERR_CUDA, "pinned host allocation failed");
+    if (!(b->h_status = static_cast<decltype(b->h_status)>(p->take(cnt, true))))
+        return fail(MARS_ERR_CUDA, "pinned host allocation failed");
+    if (!(b->d_s0 = static_cast<decltype(b->d_s0)>(p->take(cnt * n * b->s0_elem, false))))
+        return fail(MARS_ERR_CUDA, "device allocation failed");
+    if (!(b->d_temp = static_cast<decltype(b->d_temp)>(p->take(cnt * sizeof(double), false))))
+        return fail(MARS_ERR_CUDA, "device allocation failed");
+    if (!(b->d_order = static_cast<decltype(b->d_order)>(p->take(cnt * sizeof(int), false))))
+        return fail(MARS_ERR_CUDA, "device allocation failed");
+    if (!(b->d_queue = static_cast<decltype(b->d_queue)>(p->take(sizeof(int), false))))
+        return fail(MARS_ERR_CUDA, "device allocation failed");
+    if (!(b->d_status = static_cast<decltype(b->d_status)>(p->take(cnt, false))))
+        return fail(MARS_ERR_CUDA, "device allocation failed");
+    if (!(b->d_iters = static_cast<decltype(b->d_iters)>(p->take(cnt * sizeof(long long), false))))
+        return fail(MARS_ERR_CUDA, "device allocation failed");
+    if (!(b->d_elapsed = static_cast<decltype(b->d_elapsed)>(p->take(cnt * sizeof(double), false))))
+        return fail(MARS_ERR_CUDA, "device allocation failed");
+    if (!(b->d_spins = static_cast<decltype(b->d_spins)>(p->take(cnt * n, false))))
+        return fail(MARS_ERR_CUDA, "device allocation failed");
+    if (!(b->d_energy = static_cast<decltype(b->d_energy)>(p->take(cnt * sizeof(double), false))))
+        return fail(MARS_ERR_CUDA, "device allocation failed");
+    if (!(b->d_cut = static_cast<decltype(b->d_cut)>(p->take(cnt * sizeof(double), false))))
+        return fail(MARS_ERR_CUDA, "device allocation failed");
     b->best_grid = static_cast<int>(std::min<std::int64_t>((b->count + 255) / 256, 2 * p->num_sms));
     b->best_grid = std::max(b->best_grid, 1);
-    CUDA_TRY(cudaMalloc(&b->d_part_e, b->best_grid * sizeof(double)));
-    CUDA_TRY(cudaMalloc(&b->d_part_i, b->best_grid * sizeof(long long)));
-    CUDA_TRY(cudaMalloc(&b->d_best, sizeof(long long)));
+    if (!(b->d_part_e = static_cast<decltype(b->d_part_e)>(p->take(b->best_grid * sizeof(double), false))))
+        return fail(MARS_ERR_CUDA, "device allocation failed");
+    if (!(b->d_part_i = static_cast<decltype(b->d_part_i)>(p->take(b->best_grid * sizeof(long long), false))))
+        return fail(MARS_ERR_CUDA, "device allocation failed");
+    if (!(b->d_best = static_cast<decltype(b->d_best)>(p->take(sizeof(long long), false))))
+        return fail(MARS_ERR_CUDA, "device allocation failed");
     for (auto& e : b->ev) CUDA_TRY(cudaEventCreate(&e));
     // plan (host, cheap) decides the queue length and hence the grid
     b->skipped.assign(cnt, 0);
@@ -740,7 +786,8 @@ int batch_alloc(mars_batch* b) {
     b->stencil.grid = b->grid;
     b->slots = b->grid * tm;
     b->work_bytes = per_cta * b->grid;
-    CUDA_TRY(cudaMalloc(&b->d_work, std::max<std::size_t>(b->work_bytes, 16)));
+    if (!(b->d_work = static_cast<decltype(b->d_work)>(p->take(std::max<std::size_t>(b->work_bytes, 16), false))))
+        return fail(MARS_ERR_CUDA, "device allocation failed");
     if (p->kernel == MARS_KERNEL_DENSE_UMMA) {
         const std::size_t rows = relax_dense_umma_plane_rows(b->grid);
         b->umma.s_hi = static_cast<__half*>(b->d_work);
