@@ -125,6 +125,11 @@ int mars_problem_hash(const mars_problem_t* p, uint64_t* out);
 int mars_instance_hash(int32_t n, const double* J, int64_t m, const int32_t* u, const int32_t* v,
                        const double* w, const double* h, uint64_t* out);
 
+/* brute_force_ground_state (model.hpp:139, model.cpp:296-324): exhaustive 2^n Gray-code scan
+ * on the device, n <= max_n (and <= 26); ties toward the lexicographically smallest spins
+ * (-1 before +1).  Exact for integer couplings. */
+int mars_brute_force(const mars_problem_t* p, int32_t max_n, double* energy, int8_t* spins);
+
 /* All n rows of IsingProblem::row_values (model.cpp:173-182) into out[n*n] (write_matrix). */
 int mars_problem_rows(const mars_problem_t* p, double* out);
 

@@ -149,4 +149,18 @@ int ref_io_result_document(int n, const double* J, int64_t m, const int32_t* u, 
     }
 }
 
+// brute_force_ground_state (model.cpp:296-324) with its default guard and policy.
+int ref_io_brute_force(int n, const double* J, int64_t m, const int32_t* u, const int32_t* v, const double* w,
+                       const double* h, int max_n, double* energy, int8_t* spins, char* msg, int64_t msgcap) {
+    try {
+        const mars::GroundState g = mars::brute_force_ground_state(make_problem(n, J, m, u, v, w, h), max_n);
+        *energy = g.energy;
+        for (int i = 0; i < n; ++i) spins[i] = g.spins[static_cast<std::size_t>(i)];
+        return 0;
+    } catch (const std::exception& e) {
+        put(e.what(), msg, msgcap);
+        return code_of(e);
+    }
+}
+
 }  // extern "C"

@@ -5,7 +5,7 @@ hand-written sm_100a CUDA behind a C-ABI (include/mars_b200.h), with this packag
 host-side mirror of the reference's solver API (model.hpp / solvers.hpp / runner.hpp).
 """
 from .mars import (  # noqa: F401
-    BatchSpec, BatchStats, CudaError, DeviceBatch, DivergedError, Error, InputError,
+    BatchSpec, BatchStats, CudaError, GroundState, brute_force_ground_state, DeviceBatch, DivergedError, Error, InputError,
     IsingProblem, MarsParams, MarsRunPlan, Records, RunResult, RunStatus, StartMode,
     aggregate, cut_value, distributed_batch, energy, gen_ea, gen_er, gen_sk_gaussian,
     gen_sk_pm1, generate_sk, initial_state, mars_grid_count, mars_grid_temp, mars_run_count,

@@ -69,6 +69,7 @@ SIGNATURES = {
     "mars_problem_hash": (C.c_int, [vp, vp]),
     "mars_instance_hash": (C.c_int, [i32, vp, i64, vp, vp, vp, vp, vp]),
     "mars_problem_rows": (C.c_int, [vp, vp]),
+    "mars_brute_force": (C.c_int, [vp, i32, vp, vp]),
     "mars_energy": (C.c_int, [vp, vp, vp, vp]),
     "mars_validate_params": (C.c_int, [P_params]),
     "mars_run_count": (C.c_int, [P_params, i64, vp]),

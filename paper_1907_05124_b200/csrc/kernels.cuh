@@ -147,6 +147,11 @@ struct StencilLaunch {
 cudaError_t launch_relax_stencil(const RelaxArgs& a, const StencilArgs& g, const StencilLaunch& l, cudaStream_t st);
 std::size_t relax_stencil_smem(int n, int nlev, bool smem_state);
 
+// Exhaustive ground-state scan (brute_force.cu), n <= brute_force_max_n().
+int brute_force_max_n();
+cudaError_t launch_brute_force(const double* J, const double* h, int n, double* part_e, unsigned* part_key,
+                               int blocks, cudaStream_t st);
+
 cudaError_t launch_energy(const EnergyArgs& a, cudaStream_t st);
 cudaError_t launch_best(const BestArgs& a, int grid, cudaStream_t st);
 

@@ -1385,6 +1385,49 @@ int mars_run_batch(mars_problem_t* p, const mars_params_t* prm, int64_t runs, ui
     return MARS_OK;
 }
 
+// brute_force_ground_state (model.cpp:296-324): exhaustive Gray-code scan on the device
+// (brute_force.cu), ties toward the lexicographically smallest spins; the energy reported is
+// recomputed in the reference's exact order.
+int mars_brute_force(const mars_problem_t* p, int32_t max_n, double* energy_out, int8_t* spins) {
+    if (!p || !spins) return fail(MARS_ERR_INPUT, "null argument");
+    const int n = p->n;
+    if (n > max_n)
+        return fail(MARS_ERR_INPUT, "brute force refused: n = " + std::to_string(n) + " exceeds guard " +
+                                        std::to_string(max_n));
+    if (n > brute_force_max_n())
+        return fail(MARS_ERR_INPUT, "brute force supports n <= " + std::to_string(brute_force_max_n()));
+    CUDA_TRY(cudaSetDevice(p->device));
+    std::vector<double> J(static_cast<std::size_t>(n) * n, 0.0);
+    CUDA_TRY(mars_problem_rows(p, J.data()) == MARS_OK ? cudaSuccess : cudaErrorInvalidValue);
+    const int blocks = std::max(1, std::min(p->num_sms * 4, static_cast<int>(((1ull << n) + 255) / 256)));
+    double* dJ = nullptr;
+    double* dh = nullptr;
+    double* de = nullptr;
+    unsigned* dk = nullptr;
+    CUDA_TRY(cudaMalloc(&dJ, J.size() * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&dh, n * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&de, blocks * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&dk, blocks * sizeof(unsigned)));
+    CUDA_TRY(cudaMemcpyAsync(dJ, J.data(), J.size() * sizeof(double), cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(dh, p->h.data(), n * sizeof(double), cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(launch_brute_force(dJ, dh, n, de, dk, blocks, p->stream));
+    std::vector<double> e(blocks);
+    std::vector<unsigned> k(blocks);
+    CUDA_TRY(cudaMemcpyAsync(e.data(), de, blocks * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(k.data(), dk, blocks * sizeof(unsigned), cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    cudaFree(dJ);
+    cudaFree(dh);
+    cudaFree(de);
+    cudaFree(dk);
+    int best = 0;
+    for (int b = 1; b < blocks; ++b)
+        if (e[b] < e[best] || (e[b] == e[best] && k[b] < k[best])) best = b;
+    for (int i = 0; i < n; ++i)   // key = bit-reversed mask: bit (n-1-i) of the key is spin i
+        spins[i] = ((k[best] >> (n - 1 - i)) & 1u) ? 1 : -1;
+    return energy_out ? mars_energy(p, spins, energy_out, nullptr) : MARS_OK;
+}
+
 // ------------------------------------------------------------ instance generators
 
 void mars_gen_sk_gaussian(int32_t n, uint64_t seed, double* J) {           // io.cpp:151-163

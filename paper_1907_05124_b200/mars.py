@@ -275,6 +275,22 @@ def cut_value(p: IsingProblem, spins) -> float:
     return float(c[0])
 
 
+@dataclass
+class GroundState:
+    """model.hpp:131-134."""
+    energy: float
+    spins: np.ndarray
+
+
+def brute_force_ground_state(p: IsingProblem, max_n: int = 26) -> GroundState:
+    """brute_force_ground_state (model.cpp:296-324) on the device: exhaustive Gray-code scan,
+    ties toward the lexicographically smallest spins; exact for integer couplings."""
+    spins = np.zeros(p.size(), np.int8)
+    e = np.zeros(1)
+    _check(lib.mars_brute_force(p._h, int(max_n), ptr(e), ptr(spins)))
+    return GroundState(float(e[0]), spins)
+
+
 def round_spins(state) -> np.ndarray:
     """model.cpp:245-249 (host helper for tests/callers; the kernels round on device)."""
     s = np.asarray(state, np.float64)
