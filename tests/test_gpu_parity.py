@@ -331,7 +331,7 @@ def test_device_tanh_matches_libm():
 
 
 @pytest.mark.parametrize("kind", ["er_pm1", "er_gauss_field", "ea2d", "ea3d", "er_dense_storage",
-                                  "ea2d_narrow_ctas"])
+                                  "ea2d_narrow_ctas", "ea2d_field", "ea3d_grid_sweep"])
 def test_sparse_kernels_exact_vs_reference(kind, port, monkeypatch):
     """With the reference's own tanh on the device, the fp64 sparse kernels reproduce the
     reference's descents exactly: every status, iteration count, energy, cut and spin."""
@@ -351,6 +351,11 @@ def test_sparse_kernels_exact_vs_reference(kind, port, monkeypatch):
         n, (u, v, w) = 24 * 24, mb.gen_ea(24, 2, 3)
     elif kind == "ea3d":
         n, (u, v, w) = 8 ** 3, mb.gen_ea(8, 3, 4)
+    elif kind == "ea2d_field":         # stencil kernel with an external field
+        n, (u, v, w) = 20 * 20, mb.gen_ea(20, 2, 8)
+        h = rng.standard_normal(n) * 0.5
+    elif kind == "ea3d_grid_sweep":    # GridSweep plan (skipped t = 0 slot) on the stencil
+        n, (u, v, w) = 6 ** 3, mb.gen_ea(6, 3, 9)
     elif kind == "ea2d_narrow_ctas":   # levels wider than the CTA: several sites per thread
         n, (u, v, w) = 48 * 48, mb.gen_ea(48, 2, 6)
         monkeypatch.setenv("MARS_STENCIL_THREADS", "32")
@@ -359,8 +364,12 @@ def test_sparse_kernels_exact_vs_reference(kind, port, monkeypatch):
     p = mb.IsingProblem.from_edges(n, (u, v, w), h)
     assert p.kernel() == "csr"
     runs, seed, tmax = 128, 23, 8.0
-    dev = mb.run_batch(p, mb.BatchSpec(uniform(tmax), runs, seed, keep_spins=True)).records
-    ob = port.problem_edges(n, u, v, w, h).run_batch(params(0, tmax, 1, uniform=True), runs, seed)
+    if kind == "ea3d_grid_sweep":
+        prm, oprm = mb.MarsParams(0, 6, 0.25), params(0, 6, 0.25)
+    else:
+        prm, oprm = uniform(tmax), params(0, tmax, 1, uniform=True)
+    dev = mb.run_batch(p, mb.BatchSpec(prm, runs, seed, keep_spins=True)).records
+    ob = port.problem_edges(n, u, v, w, h).run_batch(oprm, runs, seed)
     assert np.array_equal(dev.status, ob.status)
     assert np.array_equal(dev.descent_iters, ob.descent_iters)
     assert np.array_equal(dev.energy.view(np.int64), ob.energy.view(np.int64))
