@@ -123,7 +123,8 @@ struct SpmmLaunch {
     int warps;
     int ring_bytes;
     int cw;                    // chunk (layout) width: 16, 32 or 64
-    int h;                     // runs per warp (1 or 2); spins per lane = cw * h / 32 (1 or 2)
+    int h;                     // lane groups per warp (1 or 2); spins per lane = cw * h / 32 (1 or 2)
+    int r;                     // runs per lane group (1, or 2 with one spin per lane), interleaved
 };
 cudaError_t launch_relax_spmm(const RelaxArgs& a, const SparseLevels& g, const SpmmLaunch& l, cudaStream_t st);
 std::size_t relax_spmm_smem(int np, int runs_per_warp, int warps, int ring_bytes);

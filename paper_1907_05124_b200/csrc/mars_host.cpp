@@ -613,24 +613,26 @@ bool spmm_config(mars_batch* b) {
     // runs per warp: two 16-lane groups for 16-wide chunks, else one run per warp
     l.h = env_int("MARS_SPMM_H", l.cw == 16 ? 2 : 1);
     if (!relax_spmm_shape_ok(l.cw, l.h)) l.h = l.cw == 16 ? 2 : 1;
+    // runs per lane group: 2 (interleaved, one 16-byte gather serves both) needs one spin per lane
+    l.r = env_int("MARS_SPMM_R", 1) == 2 && l.cw * l.h == 32 ? 2 : 1;
     // byte ring: the largest block plus ~3 average blocks in flight (MARS_SPMM_RING_KB)
     const std::size_t avg = p->nchunks ? p->chunk_bytes / p->nchunks : p->buf_bytes;
     std::size_t ring_bytes = std::max<std::size_t>(p->buf_bytes + 3 * avg, 2 * p->buf_bytes);
     if (const int kb = env_int("MARS_SPMM_RING_KB", 0)) ring_bytes = static_cast<std::size_t>(kb) * 1024;
     ring_bytes = std::max<std::size_t>((ring_bytes + 15) / 16 * 16, p->buf_bytes);
     l.ring_bytes = static_cast<int>(ring_bytes);
-    const std::size_t warp_bytes = relax_spmm_smem(p->np, l.h, 1, 0);
+    const std::size_t warp_bytes = relax_spmm_smem(p->np, l.h * l.r, 1, 0);
     if (ring_bytes + 4 * warp_bytes > kSmem && !(k && std::string(k) == "spmm")) return false;
     // CTAs per SM (each with its own ring): smaller CTAs couple fewer warps to one ring
     const int per_sm = std::max(1, env_int("MARS_SPMM_CTAS_PER_SM", 1));
     const std::size_t budget = (kSmem + 1024) / per_sm - 1024;
     int warps = static_cast<int>((budget - std::min(budget, ring_bytes)) / warp_bytes);
     warps = std::max(1, std::min({relax_spmm_max_warps(), warps, env_int("MARS_SPMM_WARPS", 64)}));
-    const int runs_per_cta = warps * l.h;
+    const int runs_per_cta = warps * l.h * l.r;
     l.warps = warps;
     l.grid = std::max(1, std::min(per_sm * p->num_sms, (b->queue_len + runs_per_cta - 1) / runs_per_cta));
     l.grid = env_int("MARS_SPARSE_GRID", l.grid);
-    return relax_spmm_smem(p->np, l.h, l.warps, l.ring_bytes) <= 227 * 1024;
+    return relax_spmm_smem(p->np, l.h * l.r, l.warps, l.ring_bytes) <= 227 * 1024;
 }
 
 int sparse_config(mars_batch* b) {
@@ -770,7 +772,7 @@ int batch_alloc(mars_batch* b) {
             max_grid = env_int("MARS_SPARSE_GRID", per_sm * p->num_sms);
             per_cta = l.smem_state ? 0 : static_cast<std::size_t>(p->np) * sizeof(double);
         } else if ((b->use_spmm = spmm_config(b))) {
-            tm = b->spmm.warps * b->spmm.h;
+            tm = b->spmm.warps * b->spmm.h * b->spmm.r;
             max_grid = b->spmm.grid;
             per_cta = 0;
         } else {

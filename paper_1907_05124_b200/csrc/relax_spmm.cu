@@ -51,16 +51,17 @@ struct RingAlloc {
     unsigned head, oldest, inflight;   // next free byte, oldest in-flight chunk index, count
 };
 
-template <int H, int K, bool UNIT>
+template <int H, int K, int R, bool UNIT>
 __global__ void __launch_bounds__((kMaxConsumerWarps + 1) * 32, 1)
 relax_spmm_kernel(RelaxArgs a, SparseLevels g, int ring_bytes) {
-    constexpr int CWR = 32 / H;        // lanes per run
+    static_assert(R == 1 || (R == 2 && K == 1), "two runs per lane group only with one spin per lane");
+    constexpr int CWR = 32 / H;        // lanes per lane group
     constexpr int CWL = CWR * K;       // spins per chunk (layout width)
     constexpr int nring = kMaxSlots;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) std::uint64_t full[kMaxSlots], empty[kMaxSlots];
     __shared__ unsigned offs[kMaxSlots];
-    __shared__ Slot slots[kMaxConsumerWarps * H];
+    __shared__ Slot slots[kMaxConsumerWarps * H * R];
     __shared__ int s_active;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int W = (blockDim.x >> 5) - 1;          // consumer warps; warp W is the producer
@@ -81,23 +82,26 @@ relax_spmm_kernel(RelaxArgs a, SparseLevels g, int ring_bytes) {
         s_active = 0;
     }
     __syncthreads();
-    const int my = warp * H + h;                  // this lane group's run slot
-    double* st = st_all + static_cast<std::size_t>(my) * np;
+    // lane group (warp, h) owns R run slots; their states are interleaved st[i][R]
+    const int my = (warp * H + h) * R;            // first run slot of this lane group
+    double* st = st_all + static_cast<std::size_t>(warp * H + h) * np * R;
     if (warp < W) {
-        if (s == 0) {
-            const int run = claim_run(a);
-            if (run >= 0) {
-                slot_start(slots[my], run, a);
-                atomicAdd(&s_active, 1);
-            } else {
-                slots[my].run = -1;
+        for (int r = 0; r < R; ++r) {
+            if (s == 0) {
+                const int run = claim_run(a);
+                if (run >= 0) {
+                    slot_start(slots[my + r], run, a);
+                    atomicAdd(&s_active, 1);
+                } else {
+                    slots[my + r].run = -1;
+                }
             }
+            __syncwarp();
+            const int run = slots[my + r].run;
+            if (run >= 0)
+                for (int i = s; i < n; i += CWR) st[static_cast<std::size_t>(i) * R + r] = s0[static_cast<std::size_t>(run) * n + i];
+            if (s == 0) st[static_cast<std::size_t>(n) * R + r] = 0.0;   // padding row
         }
-        __syncwarp();
-        const int run = slots[my].run;
-        if (run >= 0)
-            for (int i = s; i < n; i += CWR) st[i] = s0[static_cast<std::size_t>(run) * n + i];
-        if (s == 0) st[n] = 0.0;                  // padding row read by short neighbour lists
     }
     __syncthreads();
     if (s_active == 0) return;
@@ -151,10 +155,17 @@ relax_spmm_kernel(RelaxArgs a, SparseLevels g, int ring_bytes) {
                 }
             }
         } else {
-            // ---------------- consumers: one Gauss-Seidel sweep of this group's run
-            const bool act = slots[my].run >= 0;
-            const double T = slots[my].T;
-            double dmax = 0.0;
+            // ---------------- consumers: one Gauss-Seidel sweep of this group's runs
+            bool act[R];
+            double T[R], dmax[R];
+            bool any = false;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                act[r] = slots[my + r].run >= 0;
+                T[r] = slots[my + r].T;
+                dmax[r] = 0.0;
+                any |= act[r];
+            }
             long long t_wait = 0, t_sum = 0, t_trial = 0;
             for (int c = 0; c < nch; ++c) {
                 const unsigned k = q + c, slot = k % nring;
@@ -163,22 +174,36 @@ relax_spmm_kernel(RelaxArgs a, SparseLevels g, int ring_bytes) {
                 const long long t1 = a.prof ? clock64() : 0;
                 const unsigned char* cbase = ring + offs[slot];
                 const int* blk = reinterpret_cast<const int*>(cbase);
-                if (act) {
+                if (any) {
                     const int md = blk[0];                  // multiple of 4
                     int sp[K];
 #pragma unroll
                     for (int kk = 0; kk < K; ++kk) sp[kk] = blk[4 + s + CWR * kk];
                     const int* ip = blk + 4 + CWL + s;
-                    double acc[K];
+                    double acc[K][R];
 #pragma unroll
-                    for (int kk = 0; kk < K; ++kk) acc[kk] = 0.0;
+                    for (int kk = 0; kk < K; ++kk)
+#pragma unroll
+                        for (int r = 0; r < R; ++r) acc[kk][r] = 0.0;
                     if (UNIT) {
                         for (int j = 0; j < md; j += 4) {
 #pragma unroll
                             for (int u = 0; u < 4; ++u)
 #pragma unroll
-                                for (int kk = 0; kk < K; ++kk)
-                                    acc[kk] = __dadd_rn(acc[kk], signed_load(st, ip[CWL * (j + u) + CWR * kk]));
+                                for (int kk = 0; kk < K; ++kk) {
+                                    const int code = ip[CWL * (j + u) + CWR * kk];
+                                    if constexpr (R == 1) {
+                                        acc[kk][0] = __dadd_rn(acc[kk][0], signed_load(st, code));
+                                    } else {
+                                        // both runs' values of row e: one 16-byte load (code << 4
+                                        // drops the sign bit), (+-1) * v as a sign-bit flip
+                                        const double2 v = *reinterpret_cast<const double2*>(
+                                            reinterpret_cast<const char*>(st) + (static_cast<unsigned>(code) << 4));
+                                        const int sg = code & static_cast<int>(0x80000000u);
+                                        acc[kk][0] = __dadd_rn(acc[kk][0], __hiloint2double(__double2hiint(v.x) ^ sg, __double2loint(v.x)));
+                                        acc[kk][1] = __dadd_rn(acc[kk][1], __hiloint2double(__double2hiint(v.y) ^ sg, __double2loint(v.y)));
+                                    }
+                                }
                         }
                     } else {
                         const double* wp = reinterpret_cast<const double*>(cbase + ((4 + CWL + md * CWL) * 4 + 15) / 16 * 16) + s;
@@ -186,9 +211,13 @@ relax_spmm_kernel(RelaxArgs a, SparseLevels g, int ring_bytes) {
 #pragma unroll
                             for (int u = 0; u < 4; ++u)
 #pragma unroll
-                                for (int kk = 0; kk < K; ++kk)
-                                    acc[kk] = __dadd_rn(acc[kk], __dmul_rn(wp[CWL * (j + u) + CWR * kk],
-                                                                           st[ip[CWL * (j + u) + CWR * kk]]));
+                                for (int kk = 0; kk < K; ++kk) {
+                                    const double wk = wp[CWL * (j + u) + CWR * kk];
+                                    const int e = ip[CWL * (j + u) + CWR * kk];
+#pragma unroll
+                                    for (int r = 0; r < R; ++r)
+                                        acc[kk][r] = __dadd_rn(acc[kk][r], __dmul_rn(wk, st[static_cast<std::size_t>(e) * R + r]));
+                                }
                         }
                     }
                     if (a.prof) {
@@ -202,49 +231,58 @@ relax_spmm_kernel(RelaxArgs a, SparseLevels g, int ring_bytes) {
                     for (int kk = 0; kk < K; ++kk) {
                         if (sp[kk] >= 0) {
                             const double hf = a.h64 ? __ldg(a.h64 + sp[kk]) : 0.0;
-                            const double trial = tanh_trial64(__dadd_rn(acc[kk], hf), T);
-                            dmax = fmax(dmax, fabs(__dsub_rn(trial, st[sp[kk]])));
-                            st[sp[kk]] = trial;
+                            double* row = st + static_cast<std::size_t>(sp[kk]) * R;
+#pragma unroll
+                            for (int r = 0; r < R; ++r) {
+                                const double trial = tanh_trial64(__dadd_rn(acc[kk][r], hf), T[r]);
+                                dmax[r] = fmax(dmax[r], fabs(__dsub_rn(trial, row[r])));
+                                row[r] = trial;
+                            }
                         }
                     }
                 }
                 __syncwarp();                     // block consumed; this level's writes visible
-                if (a.prof && act) t_trial += clock64();
+                if (a.prof && any) t_trial += clock64();
                 if (lane == 0) umma::mbar_arrive(&empty[slot]);
             }
-            if (a.prof && lane == 0 && act) {
+            if (a.prof && lane == 0 && any) {
                 long long* pr = a.prof + static_cast<std::size_t>(blockIdx.x) * kProfSlots;
                 atomicAdd(reinterpret_cast<unsigned long long*>(pr + 0), 1ull);                 // warp-sweeps
                 atomicAdd(reinterpret_cast<unsigned long long*>(pr + 1), static_cast<unsigned long long>(t_wait));
                 atomicAdd(reinterpret_cast<unsigned long long*>(pr + 2), static_cast<unsigned long long>(t_sum));
                 atomicAdd(reinterpret_cast<unsigned long long*>(pr + 3), static_cast<unsigned long long>(t_trial));
             }
-            // sweep end: the lane group's max change, state machine, refill
+            // sweep end, per run: the lane group's max change, state machine, refill
 #pragma unroll
-            for (int o = CWR / 2; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-            int code = kSlotContinue;
-            if (act && s == 0) {
-                code = slot_after_sweep(slots[my], dmax, a);
-                if (code != kSlotContinue) slot_finish(slots[my], code, a);
-            }
-            code = __shfl_sync(0xffffffffu, code, h * CWR);
-            if (code != kSlotContinue) {               // uniform per lane group, not per warp
-                const int done = __shfl_sync(gmask, s == 0 ? slots[my].run : 0, h * CWR);
-                std::int8_t* out = a.spins + static_cast<std::size_t>(done) * n;
-                for (int i = s; i < n; i += CWR) out[i] = st[i] < 0.0 ? -1 : 1;
-                int run = -1;
-                if (s == 0) {
-                    run = claim_run(a);
-                    if (run >= 0) {
-                        slot_start(slots[my], run, a);
-                    } else {
-                        slots[my].run = -1;
-                        atomicSub(&s_active, 1);
-                    }
+            for (int r = 0; r < R; ++r) {
+                double d = dmax[r];
+#pragma unroll
+                for (int o = CWR / 2; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+                int code = kSlotContinue;
+                if (act[r] && s == 0) {
+                    code = slot_after_sweep(slots[my + r], d, a);
+                    if (code != kSlotContinue) slot_finish(slots[my + r], code, a);
                 }
-                run = __shfl_sync(gmask, run, h * CWR);
-                if (run >= 0)
-                    for (int i = s; i < n; i += CWR) st[i] = s0[static_cast<std::size_t>(run) * n + i];
+                code = __shfl_sync(0xffffffffu, code, h * CWR);
+                if (code != kSlotContinue) {               // uniform per lane group, not per warp
+                    const int done = __shfl_sync(gmask, s == 0 ? slots[my + r].run : 0, h * CWR);
+                    std::int8_t* out = a.spins + static_cast<std::size_t>(done) * n;
+                    for (int i = s; i < n; i += CWR) out[i] = st[static_cast<std::size_t>(i) * R + r] < 0.0 ? -1 : 1;
+                    int run = -1;
+                    if (s == 0) {
+                        run = claim_run(a);
+                        if (run >= 0) {
+                            slot_start(slots[my + r], run, a);
+                        } else {
+                            slots[my + r].run = -1;
+                            atomicSub(&s_active, 1);
+                        }
+                    }
+                    run = __shfl_sync(gmask, run, h * CWR);
+                    if (run >= 0)
+                        for (int i = s; i < n; i += CWR)
+                            st[static_cast<std::size_t>(i) * R + r] = s0[static_cast<std::size_t>(run) * n + i];
+                }
             }
         }
         q += nch;
@@ -253,13 +291,13 @@ relax_spmm_kernel(RelaxArgs a, SparseLevels g, int ring_bytes) {
     }
 }
 
-template <int H, int K, bool UNIT>
+template <int H, int K, int R, bool UNIT>
 cudaError_t launch_t(const RelaxArgs& a, const SparseLevels& g, const SpmmLaunch& l, cudaStream_t st) {
-    const std::size_t bytes = relax_spmm_smem(a.np, H, l.warps, l.ring_bytes);
-    cudaError_t e = cudaFuncSetAttribute(relax_spmm_kernel<H, K, UNIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const std::size_t bytes = relax_spmm_smem(a.np, H * R, l.warps, l.ring_bytes);
+    cudaError_t e = cudaFuncSetAttribute(relax_spmm_kernel<H, K, R, UNIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(bytes));
     if (e != cudaSuccess) return e;
-    relax_spmm_kernel<H, K, UNIT><<<l.grid, (l.warps + 1) * 32, bytes, st>>>(a, g, l.ring_bytes);
+    relax_spmm_kernel<H, K, R, UNIT><<<l.grid, (l.warps + 1) * 32, bytes, st>>>(a, g, l.ring_bytes);
     return cudaGetLastError();
 }
 
@@ -281,10 +319,15 @@ cudaError_t launch_relax_spmm(const RelaxArgs& a, const SparseLevels& g, const S
         !relax_spmm_shape_ok(l.cw, l.h))
         return cudaErrorInvalidValue;
     const int k = l.cw * l.h / 32;
-    if (l.h == 1 && k == 1) return g.unit ? launch_t<1, 1, true>(a, g, l, st) : launch_t<1, 1, false>(a, g, l, st);
-    if (l.h == 1 && k == 2) return g.unit ? launch_t<1, 2, true>(a, g, l, st) : launch_t<1, 2, false>(a, g, l, st);
-    if (l.h == 2 && k == 1) return g.unit ? launch_t<2, 1, true>(a, g, l, st) : launch_t<2, 1, false>(a, g, l, st);
-    return g.unit ? launch_t<2, 2, true>(a, g, l, st) : launch_t<2, 2, false>(a, g, l, st);
+    if (l.r == 2) {
+        if (k != 1) return cudaErrorInvalidValue;
+        if (l.h == 1) return g.unit ? launch_t<1, 1, 2, true>(a, g, l, st) : launch_t<1, 1, 2, false>(a, g, l, st);
+        return g.unit ? launch_t<2, 1, 2, true>(a, g, l, st) : launch_t<2, 1, 2, false>(a, g, l, st);
+    }
+    if (l.h == 1 && k == 1) return g.unit ? launch_t<1, 1, 1, true>(a, g, l, st) : launch_t<1, 1, 1, false>(a, g, l, st);
+    if (l.h == 1 && k == 2) return g.unit ? launch_t<1, 2, 1, true>(a, g, l, st) : launch_t<1, 2, 1, false>(a, g, l, st);
+    if (l.h == 2 && k == 1) return g.unit ? launch_t<2, 1, 1, true>(a, g, l, st) : launch_t<2, 1, 1, false>(a, g, l, st);
+    return g.unit ? launch_t<2, 2, 1, true>(a, g, l, st) : launch_t<2, 2, 1, false>(a, g, l, st);
 }
 
 }  // namespace marsb200

@@ -270,6 +270,10 @@ def test_sparse_launch_shapes_bit_identical(kind, monkeypatch, port):
                for wp, rg, cw, hh, gr in [("1", "1", "32", "1", "0"), ("3", "3", "16", "2", "5"),
                                           ("8", "5", "64", "1", "0"), ("2", "40", "32", "2", "0"),
                                           ("16", "8", "64", "1", "3")]]
+    # two runs per lane group, interleaved (one 16-byte gather for both)
+    shapes += [dict(MARS_SPARSE_KERNEL="spmm", MARS_SPMM_R="2", MARS_SPMM_WARPS=wp, MARS_SPARSE_CW=cw,
+                    MARS_SPMM_H=hh, MARS_SPARSE_GRID=gr)
+               for wp, cw, hh, gr in [("1", "32", "1", "0"), ("5", "16", "2", "0"), ("3", "32", "1", "4")]]
     if kind != "er_gauss":
         # torus stencil kernel: state in shared memory or a global row, any CTA width / grid
         shapes += [dict(MARS_SPARSE_KERNEL="stencil", MARS_SPARSE_STATE=st, MARS_STENCIL_THREADS=th,
@@ -279,7 +283,7 @@ def test_sparse_launch_shapes_bit_identical(kind, monkeypatch, port):
     for env in shapes:
         for k in ("MARS_SPARSE_KERNEL", "MARS_STENCIL_THREADS", "MARS_SPARSE_STATE", "MARS_SPARSE_WARPS", "MARS_SPARSE_GRID",
                   "MARS_SPARSE_R", "MARS_SPARSE_CW", "MARS_SPMM_WARPS", "MARS_SPMM_RING_KB",
-                  "MARS_SPMM_H"):
+                  "MARS_SPMM_H", "MARS_SPMM_R"):
             monkeypatch.delenv(k, raising=False)
         for k, val in env.items():
             if val == "off":
