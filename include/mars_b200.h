@@ -90,6 +90,8 @@ typedef struct {
     int64_t total_sweeps;    /* sum of descent_iters over the batch                          */
     int32_t grid;            /* CTAs of the relaxation kernel                                */
     int32_t slots;           /* concurrent descents (run slots) on the device                */
+    int32_t kernel;          /* relaxation kernel this batch ran: MARS_KERNEL_* or 4 = small  */
+    int32_t reserved;
 } mars_timing_t;
 
 typedef struct mars_problem mars_problem_t;

@@ -52,7 +52,7 @@ class mars_stats_t(C.Structure):
 class mars_timing_t(C.Structure):
     _fields_ = [("relax_ms", C.c_double), ("energy_ms", C.c_double), ("reduce_ms", C.c_double),
                 ("total_ms", C.c_double), ("launches", C.c_int64), ("total_sweeps", C.c_int64),
-                ("grid", C.c_int32), ("slots", C.c_int32)]
+                ("grid", C.c_int32), ("slots", C.c_int32), ("kernel", C.c_int32), ("reserved", C.c_int32)]
 
 
 vp, i32, i64, u64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double

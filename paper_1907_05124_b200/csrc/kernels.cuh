@@ -148,6 +148,12 @@ struct StencilLaunch {
 cudaError_t launch_relax_stencil(const RelaxArgs& a, const StencilArgs& g, const StencilLaunch& l, cudaStream_t st);
 std::size_t relax_stencil_smem(int n, int nlev, bool smem_state);
 
+// Small dense instances with integer couplings (relax_small.cu): one warp per run, J (fp16)
+// and fields on chip; for batches too small to fill the tensor-core kernel.
+cudaError_t launch_relax_small(const RelaxArgs& a, const __half* J, int grid, cudaStream_t st);
+int relax_small_max_n();
+int relax_small_slots_per_cta();
+
 // Exhaustive ground-state scan (brute_force.cu), n <= brute_force_max_n().
 int brute_force_max_n();
 cudaError_t launch_brute_force(const double* J, const double* h, int n, double* part_e, unsigned* part_key,

@@ -379,3 +379,15 @@ def test_sparse_kernels_exact_vs_reference(kind, port, monkeypatch):
     assert np.array_equal(dev.energy.view(np.int64), ob.energy.view(np.int64))
     assert np.array_equal(dev.cut.view(np.int64), ob.cut.view(np.int64))
     assert np.array_equal(dev.spins, ob.spins)
+
+
+def test_small_dense_kernel_matches_reference(monkeypatch):
+    """The opt-in on-chip small-instance kernel (MARS_DENSE_SMALL=1) on cfg1's instance: the
+    reference's full-batch records within the dense (fp32) bar, and the best energy exactly."""
+    monkeypatch.setenv("MARS_DENSE_SMALL", "1")
+    w = WORKLOADS["cfg1_sk256_pm1"]
+    g = golden("cfg1")
+    p = build_problem(w)
+    stats = mb.run_batch(p, mb.BatchSpec(w.params(), w.runs, w.base_seed, keep_spins=True))
+    compare_records(stats, g, w.n)
+    assert stats.best_energy == -6120.0
