@@ -1,4 +1,5 @@
 #!/bin/bash
+# Standard GPU validation session (run through gpurun): GPU tests, smoke(), default bench, cfg1 bench.
 mkdir -p gpurun_out/fin
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/fin/pytest_gpu.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/fin/smoke.log 2>&1
