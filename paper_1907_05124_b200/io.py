@@ -19,7 +19,6 @@ host (they are not on the hot path); problems are created on the device through 
 """
 from __future__ import annotations
 
-import ctypes as C
 import datetime
 import enum
 import json

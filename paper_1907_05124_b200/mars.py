@@ -22,7 +22,7 @@ import ctypes as C
 import enum
 import time
 from dataclasses import dataclass, field
-from typing import Callable, Optional, Sequence
+from typing import Callable, Optional
 
 import numpy as np
 
