@@ -125,6 +125,36 @@ def cpu_reference_sample(w, runs: int, workers: int):
     return runs / dt, dt, b, kind
 
 
+def pool_finish_times(elapsed, workers: int):
+    """Retirement time of each run under the reference's worker pool (runner.cpp:90-124:
+    `workers` threads claim run indices in order from an atomic counter), replayed from the
+    runs' own elapsed_seconds -- the CPU side of time-to-best."""
+    import heapq
+    import numpy as np
+    free = [0.0] * max(1, workers)
+    out = np.zeros(len(elapsed))
+    for i, e in enumerate(elapsed):
+        t = heapq.heappop(free)
+        out[i] = t + float(e)
+        heapq.heappush(free, out[i])
+    return out
+
+
+def reference_time_to_best(w, b, workers: int) -> dict:
+    """Time-to-best of a reference sample: earliest replayed retirement of a run attaining the
+    sample's best energy (hit rule runner.cpp:160-162)."""
+    import numpy as np
+    from paper_1907_05124_b200.mars import time_to_best
+    tol = 1e-9 if w.kind == "sk_gauss" else 0.0
+    ok = b.status == 0
+    best = float(b.energy[ok].min()) if ok.any() else float("nan")
+    fin = pool_finish_times(b.elapsed_seconds, workers)
+    return {"value": time_to_best(b.energy, b.status, fin, best, tol), "unit": "s",
+            "best_energy": best, "last_retirement_s": float(fin.max()) if fin.size else 0.0,
+            "clock": "per-run elapsed_seconds of the sample replayed through the reference's "
+                     "in-order worker pool"}
+
+
 def profiled_traffic(workload: str):
     """DRAM bytes (read + write) per launch of the workload's dominant kernel, from the
     committed ncu --set full capture of the same bench command (profiles/r01/ncu_summary.json),
@@ -189,6 +219,7 @@ def run_reference(args, w, rank):
         v, dt, b, kind = cpu_reference_sample(w, runs, cores)
         vals.append(v)
         secs.append(dt)
+    ttb = reference_time_to_best(w, b, cores)
     value = statistics.mean(vals)
     sample = (f"first {runs} run indices of {w.name} (same runs the GPU executes), "
               f"mars::run_batch with {cores} workers")
@@ -203,6 +234,7 @@ def run_reference(args, w, rank):
                          "sample": sample},
         "e2e": {"value": value, "unit": "descents/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "time_to_best": ttb,
     }
     print(json.dumps(line), flush=True)
 
@@ -257,6 +289,26 @@ def run_b200(args, w, rank, world, local_rank, dist):
     ok = rec.status == 0
     sweeps = int(rec.descent_iters[rec.status != 1].sum())
     best_local = float(rec.energy[ok].min()) if ok.any() else float("nan")
+    # time-to-best of the last timed step: device %globaltimer from the first
+    # descent start to the earliest retirement of a run attaining the batch-wide best energy
+    finish = batch.finish_seconds()
+    tol = problem.energy_equality_tolerance()
+    best_all = best_local
+    if dist is not None:
+        t = torch.tensor([best_all], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        best_all = float(t.item())
+    ttb = mb.time_to_best(rec.energy, rec.status, finish, best_all, tol)
+    if dist is not None:
+        t = torch.tensor([ttb], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        ttb = float(t.item())
+    ttb_line = {"value": ttb, "unit": "s", "best_energy": best_all,
+                "last_retirement_s": float(finish.max()) if finish.size else 0.0,
+                "hits": int((ok & (np.abs(rec.energy - best_all) <= tol)).sum()),
+                "clock": "device %globaltimer, last timed step, from the first descent start "
+                         "(max over ranks is not taken: ranks start together after the barrier, "
+                         "the earliest rank to hit the global best wins)"}
 
     # ---- e2e through the public API (host plan + H2D + kernels + D2H + aggregation)
     e2e = None
@@ -331,7 +383,8 @@ def run_b200(args, w, rank, world, local_rank, dist):
                    "sample": f"first {cruns} run indices of {w.name} via mars::run_batch, "
                              f"{cores} workers, {dt:.1f} s",
                    "sweep_runs_per_s": float(b.descent_iters.sum() / dt),
-                   "best_energy_sample": float(b.stats["best_energy"])}
+                   "best_energy_sample": float(b.stats["best_energy"]),
+                   "time_to_best": reference_time_to_best(w, b, cores)}
     line = {
         "metric": "descents_per_sec", "value": value, "unit": "descents/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -351,6 +404,7 @@ def run_b200(args, w, rank, world, local_rank, dist):
         "sweep_runs_per_s": sweeps * world / (ms_per_step / 1000.0),
         "mean_sweeps_per_descent": sweeps / max(1, int((rec.status != 1).sum())),
         "best_energy": best_local, "relax_ms": relax_ms, "wall_s_timed": t_wall,
+        "time_to_best": ttb_line,
     }
     print(json.dumps(line), flush=True)
 

@@ -183,6 +183,10 @@ int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing);
 /* D2H of the records (and optional per-run spins), best index and best spins. */
 int mars_batch_fetch(mars_batch_t* b, mars_records_t* records, int64_t* best_index,
                      int8_t* best_spins);
+/* Time-to-best support: per run, seconds from the launch's first descent
+ * start to that run's retirement on the device (%globaltimer); 0 for skipped runs.  No
+ * reference counterpart (the reference records only per-run elapsed_seconds). */
+int mars_batch_fetch_finish(mars_batch_t* b, double* finish_seconds);
 void mars_batch_destroy(mars_batch_t* b);
 
 /* ---- instance generators built from the reference Rng --------------- */

@@ -10,6 +10,6 @@ from .mars import (  # noqa: F401
     aggregate, cut_value, distributed_batch, energy, gen_ea, gen_er, gen_sk_gaussian,
     gen_sk_pm1, generate_sk, initial_state, mars_grid_count, mars_grid_temp, mars_run_count,
     mars_run_plan, mars_sweep, round_spins, run_batch, run_batch_with, run_shard, shard_range,
-    splitmix64, sub_seed, validate,
+    splitmix64, sub_seed, time_to_best, validate,
 )
 from . import io  # noqa: F401,E402  (instance I/O and result documents, io.hpp mirror)

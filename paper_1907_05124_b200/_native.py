@@ -85,6 +85,7 @@ SIGNATURES = {
     "mars_batch_upload": (C.c_int, [vp]),
     "mars_batch_execute": (C.c_int, [vp, C.POINTER(mars_timing_t)]),
     "mars_batch_fetch": (C.c_int, [vp, C.POINTER(mars_records_t), vp, vp]),
+    "mars_batch_fetch_finish": (C.c_int, [vp, vp]),
     "mars_batch_destroy": (None, [vp]),
     "mars_gen_sk_gaussian": (None, [i32, u64, vp]),
     "mars_gen_sk_pm1": (None, [i32, u64, vp]),

@@ -37,6 +37,7 @@ struct RelaxArgs {
     std::uint8_t* status;
     long long* iters;
     double* elapsed;
+    unsigned long long* done_ns;  // [count] %globaltimer when the run retired, or nullptr
     std::int8_t* spins;        // [count][n] rounded final state (round_spins, model.cpp:245)
     // optional per-CTA phase counters (clock64 cycles), kProfSlots per CTA, or nullptr
     long long* prof;

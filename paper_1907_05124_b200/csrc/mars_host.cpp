@@ -550,6 +550,7 @@ struct mars_batch {
     std::uint8_t* d_status = nullptr;
     long long* d_iters = nullptr;
     double* d_elapsed = nullptr;
+    unsigned long long* d_done = nullptr;  // [count] retirement %globaltimer (time-to-best)
     std::int8_t* d_spins = nullptr;
     double* d_energy = nullptr;
     double* d_cut = nullptr;
@@ -575,7 +576,7 @@ struct mars_batch {
             p->give(h, true);
         for (void* d : {d_s0, static_cast<void*>(d_temp), static_cast<void*>(d_order), d_work,
                         static_cast<void*>(d_queue), static_cast<void*>(d_status), static_cast<void*>(d_iters),
-                        static_cast<void*>(d_elapsed), static_cast<void*>(d_spins), static_cast<void*>(d_energy),
+                        static_cast<void*>(d_elapsed), static_cast<void*>(d_done), static_cast<void*>(d_spins), static_cast<void*>(d_energy),
                         static_cast<void*>(d_cut), static_cast<void*>(d_part_e), static_cast<void*>(d_part_i),
                         static_cast<void*>(d_best)})
             p->give(d, false);
@@ -702,6 +703,8 @@ int batch_alloc(mars_batch* b) {
     if (!(b->d_iters = static_cast<decltype(b->d_iters)>(p->take(cnt * sizeof(long long), false))))
         return fail(MARS_ERR_CUDA, "device allocation failed");
     if (!(b->d_elapsed = static_cast<decltype(b->d_elapsed)>(p->take(cnt * sizeof(double), false))))
+        return fail(MARS_ERR_CUDA, "device allocation failed");
+    if (!(b->d_done = static_cast<decltype(b->d_done)>(p->take(cnt * sizeof(unsigned long long), false))))
         return fail(MARS_ERR_CUDA, "device allocation failed");
     if (!(b->d_spins = static_cast<decltype(b->d_spins)>(p->take(cnt * n, false))))
         return fail(MARS_ERR_CUDA, "device allocation failed");
@@ -1170,6 +1173,7 @@ int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
     ra.status = b->d_status;
     ra.iters = b->d_iters;
     ra.elapsed = b->d_elapsed;
+    ra.done_ns = b->d_done;
     ra.spins = b->d_spins;
     std::int64_t launches = 0;
     const bool prof = std::getenv("MARS_PROFILE") != nullptr;
@@ -1303,6 +1307,37 @@ int mars_batch_fetch(mars_batch_t* b, mars_records_t* rec, int64_t* best_index,
         }
     }
     if (best_index) *best_index = best < 0 ? -1 : b->first + best;
+    return MARS_OK;
+}
+
+int mars_batch_fetch_finish(mars_batch_t* b, double* finish_seconds) {
+    if (!b || !finish_seconds) return fail(MARS_ERR_INPUT, "null argument");
+    if (!b->executed) return fail(MARS_ERR_RUNTIME, "batch fetched before execute");
+    mars_problem* p = b->p;
+    cudaStream_t st = p->stream;
+    const std::size_t cnt = static_cast<std::size_t>(b->count);
+    if (!cnt) return MARS_OK;
+    CUDA_TRY(cudaSetDevice(p->device));
+    std::vector<std::uint8_t> status(cnt);
+    std::vector<double> elapsed(cnt);
+    std::vector<unsigned long long> done(cnt);
+    CUDA_TRY(cudaMemcpyAsync(status.data(), b->d_status, cnt, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(elapsed.data(), b->d_elapsed, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(done.data(), b->d_done, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    // origin = the earliest descent start of the launch (retirement - its own elapsed)
+    long double origin = 0.0L;
+    bool any = false;
+    for (std::size_t k = 0; k < cnt; ++k) {
+        if (status[k] > MARS_RUN_DIVERGED || status[k] == MARS_RUN_SKIPPED) continue;
+        const long double t0 = static_cast<long double>(done[k]) - 1e9L * elapsed[k];
+        if (!any || t0 < origin) origin = t0;
+        any = true;
+    }
+    for (std::size_t k = 0; k < cnt; ++k) {
+        const bool ran = status[k] <= MARS_RUN_DIVERGED && status[k] != MARS_RUN_SKIPPED;
+        finish_seconds[k] = ran ? static_cast<double>((static_cast<long double>(done[k]) - origin) * 1e-9L) : 0.0;
+    }
     return MARS_OK;
 }
 

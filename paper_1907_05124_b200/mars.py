@@ -642,3 +642,19 @@ class DeviceBatch:
         spins = np.zeros(self.problem.size(), np.int8)
         _check(lib.mars_batch_fetch(self._b, C.byref(c), ptr(best), ptr(spins)))
         return rec, int(best[0]), spins
+
+    def finish_seconds(self) -> np.ndarray:
+        """Per run: seconds from the launch's first descent start to the run's retirement
+        (device %globaltimer of the last ``execute``; 0 for skipped runs)."""
+        out = np.zeros(self.count, np.float64)
+        _check(lib.mars_batch_fetch_finish(self._b, ptr(out)))
+        return out
+
+
+def time_to_best(energy: np.ndarray, status: np.ndarray, finish: np.ndarray, best: float,
+                 tol: float = 0.0) -> float:
+    """Time-to-best: the earliest retirement among the completed runs whose
+    energy is within ``tol`` of ``best`` (the reference's hit rule, runner.cpp:160-162);
+    inf when none of these runs reaches it."""
+    hit = (status == 0) & (np.abs(energy - best) <= tol)
+    return float(finish[hit].min()) if hit.any() else float("inf")

@@ -26,3 +26,25 @@ def test_reference_arm_line():
         assert k in d, k
     assert d["impl"] == "reference" and d["unit"] == "descents/s" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] in ("reference", "port")
+    ttb = d["time_to_best"]
+    assert ttb["unit"] == "s" and 0 < ttb["value"] <= ttb["last_retirement_s"]
+
+
+def test_pool_finish_times_replays_in_order_claims():
+    import numpy as np
+    import bench
+    # 2 workers claim 0,1 at t=0; run 2 goes to whichever frees first (run 1 at 1.0)
+    fin = bench.pool_finish_times(np.array([3.0, 1.0, 1.0, 0.5]), 2)
+    assert fin.tolist() == [3.0, 1.0, 2.0, 2.5]
+    assert bench.pool_finish_times(np.array([1.0, 2.0]), 1).tolist() == [1.0, 3.0]
+
+
+def test_time_to_best_hit_rule():
+    import numpy as np
+    from paper_1907_05124_b200.mars import time_to_best
+    e = np.array([-5.0, -7.0, -7.0, -7.0 + 1e-12, -8.0])
+    st = np.array([0, 0, 0, 0, 2], np.uint8)           # the -8 run diverged: not a hit
+    fin = np.array([1.0, 4.0, 3.0, 2.0, 0.5])
+    assert time_to_best(e, st, fin, -7.0, 0.0) == 3.0
+    assert time_to_best(e, st, fin, -7.0, 1e-9) == 2.0
+    assert time_to_best(e, st, fin, -9.0, 0.0) == float("inf")

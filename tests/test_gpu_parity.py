@@ -391,3 +391,25 @@ def test_small_dense_kernel_matches_reference(monkeypatch):
     stats = mb.run_batch(p, mb.BatchSpec(w.params(), w.runs, w.base_seed, keep_spins=True))
     compare_records(stats, g, w.n)
     assert stats.best_energy == -6120.0
+
+
+@pytest.mark.parametrize("kernel", ["dense_umma", "csr"])
+def test_finish_times_for_time_to_best(kernel):
+    """mars_batch_fetch_finish: per-run retirement on the device clock, measured from the
+    launch's first descent start -- every executed run retires no earlier than its own
+    elapsed time and no later than the relaxation kernel lasted."""
+    w = WORKLOADS["cfg1_sk256_pm1"]
+    p = build_problem(w, kernel=kernel)
+    spec = mb.BatchSpec(w.params(), 512, w.base_seed)
+    b = mb.DeviceBatch(p, spec)
+    b.upload()
+    t = b.execute()
+    rec, _, _ = b.fetch()
+    fin = b.finish_seconds()
+    ran = rec.status != 1
+    assert ran.all()
+    assert np.all(fin[ran] >= rec.elapsed_seconds[ran] - 1e-6)
+    assert fin.min() >= 0.0 and fin.max() <= t["relax_ms"] * 1e-3 * 1.05 + 1e-4
+    best = float(rec.energy[rec.status == 0].min())
+    ttb = mb.time_to_best(rec.energy, rec.status, fin, best, p.energy_equality_tolerance())
+    assert 0.0 < ttb <= fin.max()
