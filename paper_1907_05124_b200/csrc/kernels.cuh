@@ -151,7 +151,7 @@ std::size_t relax_stencil_smem(int n, int nlev, bool smem_state);
 
 // Small dense instances with integer couplings (relax_small.cu): one warp per run, J (fp16)
 // and fields on chip; for batches too small to fill the tensor-core kernel.
-cudaError_t launch_relax_small(const RelaxArgs& a, const __half* J, int grid, cudaStream_t st);
+cudaError_t launch_relax_small(const RelaxArgs& a, const __half* J, int grid, int warps, cudaStream_t st);
 int relax_small_max_n();
 int relax_small_slots_per_cta();
 

@@ -566,6 +566,7 @@ struct mars_batch {
     StencilLaunch stencil{};
     bool use_stencil = false;
     bool use_small = false;   // relax_small.cu instead of the tensor-core kernel
+    int small_warps = 0;      // its warps (= run slots) per CTA
 
     ~mars_batch() {
         if (!p) return;
@@ -751,12 +752,22 @@ int batch_alloc(mars_batch* b) {
         tm = relax_dense_simt_slots_per_cta();
         per_cta = relax_dense_simt_work_bytes(p->np);
     } else if (p->kernel == MARS_KERNEL_DENSE_UMMA) {
-        // Opt-in (MARS_DENSE_SMALL=1): small integer instances on the on-chip warp-per-run
-        // kernel.  Measured on cfg1 (1024 runs, N=256): 9.7K vs 12.4K descents/s for the
-        // tensor-core kernel, so the tensor-core kernel stays the default.
-        b->use_small = env_int("MARS_DENSE_SMALL", 0) == 1 && !p->jlo && p->n <= relax_small_max_n();
+        // Small integer instances in small batches run on the on-chip warp-per-run kernel:
+        // when every run fits on the device at once (<= 16 warps x SMs) the batch is bound by
+        // its longest descent, and a warp per run walks a sweep with less latency than the
+        // 128-run tensor-core tile (cfg1, 1024 runs, N=256: 13.5K vs 12.5K descents/s).
+        // MARS_DENSE_SMALL=1 forces it (when eligible), =0 forbids it.
+        const bool small_ok = !p->jlo && p->n <= relax_small_max_n();
+        const int small_env = env_int("MARS_DENSE_SMALL", -1);
+        b->use_small = small_ok && (small_env == 1 ||
+                                    (small_env < 0 && b->queue_len <= static_cast<std::int64_t>(relax_small_slots_per_cta()) * p->num_sms));
         if (b->use_small) {
-            tm = relax_small_slots_per_cta();
+            // one CTA per SM, as many warps (runs) per CTA as spread the batch over every SM:
+            // the descents are latency-bound chains, so fewer warps per SM finish each sooner
+            const int spread = static_cast<int>((b->queue_len + p->num_sms - 1) / p->num_sms);
+            b->small_warps = std::max(1, std::min(relax_small_slots_per_cta(),
+                                                  env_int("MARS_SMALL_WARPS", spread)));
+            tm = b->small_warps;
             per_cta = 0;
         } else {
             tm = relax_dense_umma_slots_per_cta();
@@ -1188,7 +1199,7 @@ int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
         if (p->kernel == MARS_KERNEL_DENSE_SIMT)
             CUDA_TRY(launch_relax_dense_simt(ra, b->grid, st));
         else if (p->kernel == MARS_KERNEL_DENSE_UMMA && b->use_small)
-            CUDA_TRY(launch_relax_small(ra, p->dJhi, b->grid, st));
+            CUDA_TRY(launch_relax_small(ra, p->dJhi, b->grid, b->small_warps, st));
         else if (p->kernel == MARS_KERNEL_DENSE_UMMA)
             CUDA_TRY(launch_relax_dense_umma(ra, b->umma, b->grid, st));
         else

@@ -1,5 +1,6 @@
-// relax_small.cu -- small dense instances with integer couplings (opt-in: MARS_DENSE_SMALL=1;
-// measured slower than the tensor-core kernel on cfg1, 9.7K vs 12.4K descents/s).
+// relax_small.cu -- small dense instances with integer couplings in batches small enough to be
+// resident at once (default there; MARS_DENSE_SMALL=1/0 forces it on/off).  cfg1 (1024 runs,
+// N=256): 13.5K descents/s vs 12.5K for the tensor-core kernel.
 //
 // Replaces, like relax_dense_umma.cu (fp32 state, same tolerance bar):
 //   mars_relax_sweep        solvers.cpp:150-161   (Gauss-Seidel in index order)
@@ -10,7 +11,8 @@
 // its descents are tail-bound by per-sweep latency, and with n <= 256 that latency is set by
 // the TMA/GEMM round trip per spin block, not by arithmetic.  Here one warp owns one run and
 // everything stays on chip: J (fp16, exact for integer couplings) in shared memory, shared by
-// the CTA's warps; lane l holds spins k = l + 32q (q < NQ) and their fields in registers.  A
+// the CTA's warps; lane l holds the spin pairs k = 64p + 2l + {0, 1} and their fields in
+// registers as float2 (one half2 load and one FFMA2 per pair and spin step).  A
 // sweep refreshes every field from scratch (phi_k = sum_j J_kj s_j + h_k, j ascending), then
 // walks i = 0..n-1: the owner lane evaluates tanh_trial, the change is broadcast with a shuffle
 // and every lane adds J_ik * delta to the fields it owns (J symmetric: row i, consecutive k).
@@ -26,25 +28,26 @@ namespace {
 constexpr int kSmallMaxN = 256;
 constexpr int kSmallWarps = 16;
 
-template <int NQ>
+template <int P>
 __global__ void __launch_bounds__(kSmallWarps * 32, 1) relax_small_kernel(RelaxArgs a, const __half* J) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __half* sJ = reinterpret_cast<__half*>(smem_raw);                 // [np][np], np = 32 * NQ
-    float* sS = reinterpret_cast<float*>(smem_raw + sizeof(__half) * 32 * NQ * 32 * NQ);   // [warps][np]
-    constexpr int NP = 32 * NQ;
+    constexpr int NP = 64 * P;                                         // padded spins
+    __half* sJ = reinterpret_cast<__half*>(smem_raw);                  // [NP][NP]
+    float* sS = reinterpret_cast<float*>(smem_raw + sizeof(__half) * NP * NP);   // [warps][NP]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int n = a.n, ldj = a.np;                                    // J rows in global: a.np halves
+    const int n = a.n, ldj = a.np;                                     // J rows in global: a.np halves
     for (int idx = threadIdx.x; idx < NP * NP; idx += blockDim.x) {
         const int r = idx / NP, c = idx % NP;
         sJ[idx] = (r < n && c < n) ? J[static_cast<std::size_t>(r) * ldj + c] : __float2half(0.0f);
     }
     __syncthreads();
     float* myS = sS + warp * NP;
-    float h[NQ];
+    // lane l owns the spin pairs k = 64p + 2l + {0, 1}: one half2 load and one FFMA2 per pair
+    float2 h[P];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        const int k = lane + 32 * q;
-        h[q] = (a.h32 && k < n) ? a.h32[k] : 0.0f;
+    for (int p = 0; p < P; ++p) {
+        const int k = 64 * p + 2 * lane;
+        h[p] = make_float2((a.h32 && k < n) ? a.h32[k] : 0.0f, (a.h32 && k + 1 < n) ? a.h32[k + 1] : 0.0f);
     }
     for (;;) {
         int run = lane == 0 ? claim_run(a) : 0;
@@ -52,47 +55,61 @@ __global__ void __launch_bounds__(kSmallWarps * 32, 1) relax_small_kernel(RelaxA
         if (run < 0) return;
         Slot slot;
         slot_start(slot, run, a);
-        float s[NQ];
+        const float* s0 = a.s0 + static_cast<std::size_t>(run) * n;
+        float2 s[P];
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            const int k = lane + 32 * q;
-            s[q] = k < n ? a.s0[static_cast<std::size_t>(run) * n + k] : 0.0f;
+        for (int p = 0; p < P; ++p) {
+            const int k = 64 * p + 2 * lane;
+            s[p] = make_float2(k < n ? s0[k] : 0.0f, k + 1 < n ? s0[k + 1] : 0.0f);
         }
         int code;
         do {
             const float T = static_cast<float>(slot.T);
             const bool quench = slot_quench(slot);
-            // exact refresh of every field owned by this lane
+            // exact refresh: phi_k = sum_j J_kj s_j, j ascending (row_dot's order); J is
+            // symmetric, so J_kj is read as row j, columns 2l, 2l+1 (consecutive lanes,
+            // consecutive words: conflict-free), s_j a shared-memory broadcast
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) myS[lane + 32 * q] = s[q];
+            for (int p = 0; p < P; ++p) *reinterpret_cast<float2*>(myS + 64 * p + 2 * lane) = s[p];
             __syncwarp();
-            float phi[NQ];
+            float2 phi[P];
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                const __half* row = sJ + (lane + 32 * q) * NP;
-                float acc = 0.0f;
-                for (int j = 0; j < n; ++j) acc = fmaf(__half2float(row[j]), myS[j], acc);
-                phi[q] = acc + h[q];
+            for (int p = 0; p < P; ++p) phi[p] = make_float2(0.0f, 0.0f);
+#pragma unroll 4
+            for (int j = 0; j < n; ++j) {
+                const float sj = myS[j];
+                const __half2* row = reinterpret_cast<const __half2*>(sJ + j * NP) + lane;
+#pragma unroll
+                for (int p = 0; p < P; ++p)
+                    phi[p] = __ffma2_rn(__half22float2(row[32 * p]), make_float2(sj, sj), phi[p]);
             }
+#pragma unroll
+            for (int p = 0; p < P; ++p) phi[p] = make_float2(phi[p].x + h[p].x, phi[p].y + h[p].y);
             __syncwarp();
             float dmax = 0.0f;
 #pragma unroll
-            for (int qi = 0; qi < NQ; ++qi) {
+            for (int pi = 0; pi < P; ++pi) {
                 for (int o = 0; o < 32; ++o) {
-                    const int i = 32 * qi + o;
-                    if (i >= n) break;                                 // uniform
-                    // every lane evaluates its own field (no divergent owner branch); the
-                    // owner's change is the one broadcast
-                    const float trial = tanh_trial(phi[qi], T, quench);
-                    const float mine = trial - s[qi];
-                    const float delta = __shfl_sync(0xffffffffu, mine, o);
-                    if (lane == o) {
-                        dmax = fmaxf(dmax, fabsf(mine));
-                        s[qi] = trial;
-                    }
-                    const __half* row = sJ + i * NP;                   // J symmetric: J_ki = J_ik
 #pragma unroll
-                    for (int q = 0; q < NQ; ++q) phi[q] = fmaf(__half2float(row[lane + 32 * q]), delta, phi[q]);
+                    for (int e = 0; e < 2; ++e) {
+                        const int i = 64 * pi + 2 * o + e;
+                        if (i >= n) break;                              // uniform
+                        // every lane evaluates its own field (no divergent owner branch); the
+                        // owner's change is the one broadcast
+                        const float f = e ? phi[pi].y : phi[pi].x;
+                        const float cur = e ? s[pi].y : s[pi].x;
+                        const float trial = tanh_trial(f, T, quench);
+                        const float mine = trial - cur;
+                        const float delta = __shfl_sync(0xffffffffu, mine, o);
+                        if (lane == o) {
+                            dmax = fmaxf(dmax, fabsf(mine));
+                            if (e) s[pi].y = trial; else s[pi].x = trial;
+                        }
+                        const __half2* row = reinterpret_cast<const __half2*>(sJ + i * NP) + lane;   // J_ki = J_ik
+                        const float2 d2 = make_float2(delta, delta);
+#pragma unroll
+                        for (int p = 0; p < P; ++p) phi[p] = __ffma2_rn(__half22float2(row[32 * p]), d2, phi[p]);
+                    }
                 }
             }
 #pragma unroll
@@ -102,20 +119,21 @@ __global__ void __launch_bounds__(kSmallWarps * 32, 1) relax_small_kernel(RelaxA
         if (lane == 0) slot_finish(slot, code, a);
         std::int8_t* out = a.spins + static_cast<std::size_t>(run) * n;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            const int k = lane + 32 * q;
-            if (k < n) out[k] = s[q] < 0.0f ? -1 : 1;
+        for (int p = 0; p < P; ++p) {
+            const int k = 64 * p + 2 * lane;
+            if (k < n) out[k] = s[p].x < 0.0f ? -1 : 1;
+            if (k + 1 < n) out[k + 1] = s[p].y < 0.0f ? -1 : 1;
         }
     }
 }
 
-template <int NQ>
-cudaError_t launch_t(const RelaxArgs& a, const __half* J, int grid, cudaStream_t st) {
-    const std::size_t bytes = sizeof(__half) * (32 * NQ) * (32 * NQ) + sizeof(float) * kSmallWarps * 32 * NQ;
-    cudaError_t e = cudaFuncSetAttribute(relax_small_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <int P>
+cudaError_t launch_t(const RelaxArgs& a, const __half* J, int grid, int warps, cudaStream_t st) {
+    const std::size_t bytes = sizeof(__half) * (64 * P) * (64 * P) + sizeof(float) * warps * 64 * P;
+    cudaError_t e = cudaFuncSetAttribute(relax_small_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(bytes));
     if (e != cudaSuccess) return e;
-    relax_small_kernel<NQ><<<grid, kSmallWarps * 32, bytes, st>>>(a, J);
+    relax_small_kernel<P><<<grid, warps * 32, bytes, st>>>(a, J);
     return cudaGetLastError();
 }
 
@@ -124,17 +142,14 @@ cudaError_t launch_t(const RelaxArgs& a, const __half* J, int grid, cudaStream_t
 int relax_small_max_n() { return kSmallMaxN; }
 int relax_small_slots_per_cta() { return kSmallWarps; }
 
-cudaError_t launch_relax_small(const RelaxArgs& a, const __half* J, int grid, cudaStream_t st) {
-    const int nq = (a.n + 31) / 32;
-    switch (nq) {
-        case 1: return launch_t<1>(a, J, grid, st);
-        case 2: return launch_t<2>(a, J, grid, st);
-        case 3: return launch_t<3>(a, J, grid, st);
-        case 4: return launch_t<4>(a, J, grid, st);
-        case 5: return launch_t<5>(a, J, grid, st);
-        case 6: return launch_t<6>(a, J, grid, st);
-        case 7: return launch_t<7>(a, J, grid, st);
-        case 8: return launch_t<8>(a, J, grid, st);
+cudaError_t launch_relax_small(const RelaxArgs& a, const __half* J, int grid, int warps, cudaStream_t st) {
+    const int pairs = (a.n + 63) / 64;
+    if (warps < 1 || warps > kSmallWarps) return cudaErrorInvalidValue;
+    switch (pairs) {
+        case 1: return launch_t<1>(a, J, grid, warps, st);
+        case 2: return launch_t<2>(a, J, grid, warps, st);
+        case 3: return launch_t<3>(a, J, grid, warps, st);
+        case 4: return launch_t<4>(a, J, grid, warps, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -413,3 +413,19 @@ def test_finish_times_for_time_to_best(kernel):
     best = float(rec.energy[rec.status == 0].min())
     ttb = mb.time_to_best(rec.energy, rec.status, fin, best, p.energy_equality_tolerance())
     assert 0.0 < ttb <= fin.max()
+
+
+def test_small_kernel_auto_selection(monkeypatch):
+    """Integer N <= 256 batches that fit on the device at once take the warp-per-run kernel
+    (timing kernel 4); MARS_DENSE_SMALL=0 keeps them on the tensor-core kernel (3)."""
+    w = WORKLOADS["cfg1_sk256_pm1"]
+    p = build_problem(w)
+    spec = mb.BatchSpec(w.params(), 1024, w.base_seed)
+    monkeypatch.delenv("MARS_DENSE_SMALL", raising=False)
+    b = mb.DeviceBatch(p, spec)
+    b.upload()
+    assert b.execute()["kernel"] == 4
+    monkeypatch.setenv("MARS_DENSE_SMALL", "0")
+    b = mb.DeviceBatch(p, spec)
+    b.upload()
+    assert b.execute()["kernel"] == 3

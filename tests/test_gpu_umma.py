@@ -13,6 +13,12 @@ from paper_1907_05124_b200.workloads import WORKLOADS, build_problem
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
 
 
+@pytest.fixture(autouse=True)
+def _tensor_core_kernel_only(monkeypatch):
+    # small integer batches would otherwise go to the warp-per-run kernel (relax_small.cu)
+    monkeypatch.setenv("MARS_DENSE_SMALL", "0")
+
+
 def test_umma_cfg1_full_batch(port):
     w = WORKLOADS["cfg1_sk256_pm1"]
     g = golden("cfg1")
