@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, 1) relax_small_kernel(RelaxA
         do {
             const float T = static_cast<float>(slot.T);
             const bool quench = slot_quench(slot);
+            const float rT = quench ? 0.0f : recip_for_div(T);
             // exact refresh: phi_k = sum_j J_kj s_j, j ascending (row_dot's order); J is
             // symmetric, so J_kj is read as row j, columns 2l, 2l+1 (consecutive lanes,
             // consecutive words: conflict-free), s_j a shared-memory broadcast
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, 1) relax_small_kernel(RelaxA
                         // owner's change is the one broadcast
                         const float f = e ? phi[pi].y : phi[pi].x;
                         const float cur = e ? s[pi].y : s[pi].x;
-                        const float trial = tanh_trial(f, T, quench);
+                        const float trial = tanh_trial_r(f, T, rT, quench);
                         const float mine = trial - cur;
                         const float delta = __shfl_sync(0xffffffffu, mine, o);
                         if (lane == o) {
