@@ -349,6 +349,10 @@ def run_b200(args, w, rank, world, local_rank, dist):
                 "kernel": f"relax_{kname}",
                 "peak_source": f"{src} bf16 sustained (MEASURED_PEAKS.json)",
                 "algorithmic": "2*N^2 flops per sweep-run x total sweeps per launch"}
+        if kname == "dense_small":
+            roof["note"] = ("warp-per-run CUDA-core kernel for a batch resident at once: the time is the "
+                            "longest descent's serial per-spin chain (div + tanhf + shuffle), so this "
+                            "tensor fraction does not bind (DESIGN.md K1'')")
     else:
         # SpMV model of one sweep-run: each stored coupling reads one fp64 neighbour value and
         # one 4-byte index, each spin reads and writes its own fp64 value
