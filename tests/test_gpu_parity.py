@@ -429,3 +429,28 @@ def test_small_kernel_auto_selection(monkeypatch):
     b = mb.DeviceBatch(p, spec)
     b.upload()
     assert b.execute()["kernel"] == 3
+
+
+@pytest.mark.parametrize("n,h", [(37, False), (100, True), (200, False), (256, True)])
+def test_small_kernel_ragged_sizes_match_port(port, n, h):
+    """relax_small.cu (the default for these resident integer batches) at sizes that leave a
+    partial spin pair / partial 64-spin group, with and without an external field: the
+    oracle's records within the dense bar, energies bit-exact where the spins agree."""
+    from oracle.oracle import params
+    J = port.gen_sk_pm1(n, 40 + n)
+    hv = np.where(np.arange(n) % 3 == 0, 1.0, -1.0) if h else None
+    t = float(int(np.sqrt(n)) + 2)
+    ob = (port.problem_dense(J, hv) if h else port.problem_dense(J)).run_batch(
+        params(0, t, 1, 1, 1e-4, uniform=True), 256, 3)
+    p = mb.IsingProblem.dense(n, J, hv)
+    spec = mb.BatchSpec(mb.MarsParams(0, t, 1, 1, 1e-4, mb.StartMode.UniformRandom), 256, 3, keep_spins=True)
+    b = mb.DeviceBatch(p, spec)
+    b.upload()
+    assert b.execute()["kernel"] == 4
+    stats = mb.run_batch(p, spec)
+    assert np.array_equal(stats.records.status, ob.status)
+    same = np.all(stats.records.spins == ob.spins, axis=1)
+    assert same.mean() >= 0.95, same.mean()
+    assert np.array_equal(stats.records.energy[same], ob.energy[same])
+    if same.all():
+        assert stats.best_energy == ob.stats["best_energy"]
