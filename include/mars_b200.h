@@ -116,6 +116,8 @@ int mars_problem_from_edges(int32_t n, int64_t m, const int32_t* u, const int32_
                             const double* w, const double* h, int32_t device, int32_t kernel,
                             mars_problem_t** out);
 
+/* Staged batches (mars_batch_*) keep their problem alive: with batches outstanding the
+ * handle is only marked released and is freed by the last mars_batch_destroy. */
 void mars_problem_destroy(mars_problem_t* p);
 int mars_problem_info(const mars_problem_t* p, mars_problem_info_t* out);
 

@@ -6,6 +6,7 @@
 //   IsingProblem construction+metadata  model.cpp:20-131
 //   run_batch / run_batch_with          runner.cpp:81-178 (aggregation 126-167)
 // The per-run work itself (descents, energies, best-of-R) runs in the sm_100a kernels.
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -104,6 +105,10 @@ void plan_of(const mars_params_t* prm, std::uint64_t base, std::int64_t idx, boo
 // ============================================================================ problem store
 
 struct mars_problem {
+    // staged batches borrow this problem's stream and buffer pool: mars_problem_destroy
+    // with batches alive only marks the handle released, the last mars_batch_destroy frees it
+    std::atomic<int> live_batches{0};
+    std::atomic<bool> released{false};
     int n = 0;
     bool dense = true;              // storage choice of the reference (model.cpp:91)
     bool integral = true;
@@ -1056,7 +1061,11 @@ int mars_problem_rows(const mars_problem_t* p, double* out) {
     return MARS_OK;
 }
 
-void mars_problem_destroy(mars_problem_t* p) { delete p; }
+void mars_problem_destroy(mars_problem_t* p) {
+    if (!p) return;
+    p->released = true;
+    if (p->live_batches.load() == 0) delete p;
+}
 
 int mars_problem_info(const mars_problem_t* p, mars_problem_info_t* out) {
     if (!p || !out) return fail(MARS_ERR_INPUT, "null argument");
@@ -1109,6 +1118,7 @@ int mars_batch_create(mars_problem_t* p, const mars_params_t* prm, int64_t runs,
                                         std::to_string(total) + " runs");
     auto* b = new mars_batch;
     b->p = p;
+    ++p->live_batches;
     b->prm = *prm;
     if (b->prm.sweep_cap == 0) b->prm.sweep_cap = kSweepCap;
     b->runs = total;
@@ -1116,7 +1126,7 @@ int mars_batch_create(mars_problem_t* p, const mars_params_t* prm, int64_t runs,
     b->first = first;
     b->count = count;
     if (int rc = batch_alloc(b)) {
-        delete b;
+        mars_batch_destroy(b);
         return rc;
     }
     *out = b;
@@ -1352,7 +1362,12 @@ int mars_batch_fetch_finish(mars_batch_t* b, double* finish_seconds) {
     return MARS_OK;
 }
 
-void mars_batch_destroy(mars_batch_t* b) { delete b; }
+void mars_batch_destroy(mars_batch_t* b) {
+    if (!b) return;
+    mars_problem* p = b->p;
+    delete b;
+    if (p && --p->live_batches == 0 && p->released) delete p;
+}
 
 // runner.cpp:126-167 -- index-order aggregation; the all-failed batch is an error (153-155)
 int mars_aggregate(int64_t count, const uint8_t* status, const double* energy, const double* cut,

@@ -454,3 +454,20 @@ def test_small_kernel_ragged_sizes_match_port(port, n, h):
     assert np.array_equal(stats.records.energy[same], ob.energy[same])
     if same.all():
         assert stats.best_energy == ob.stats["best_energy"]
+
+
+def test_batch_outlives_destroyed_problem():
+    """mars_problem_destroy with a staged batch outstanding only marks the handle released;
+    the batch keeps executing on it and the last mars_batch_destroy frees it (the Python
+    cyclic GC may finalise a problem before a batch that references it)."""
+    from paper_1907_05124_b200._native import lib
+    w = WORKLOADS["cfg1_sk256_pm1"]
+    p = build_problem(w)
+    b = mb.DeviceBatch(p, mb.BatchSpec(w.params(), 64, w.base_seed))
+    lib.mars_problem_destroy(p._h)
+    p._h = None
+    b.upload()
+    b.execute()
+    rec, best, _ = b.fetch()
+    assert (rec.status == 0).all() and 0 <= best < 64
+    del b
