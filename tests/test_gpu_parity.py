@@ -431,7 +431,7 @@ def test_small_kernel_auto_selection(monkeypatch):
     assert b.execute()["kernel"] == 3
 
 
-@pytest.mark.parametrize("n,h", [(37, False), (100, True), (200, False), (256, True)])
+@pytest.mark.parametrize("n,h", [(37, False), (100, True), (150, False), (200, False), (256, True)])
 def test_small_kernel_ragged_sizes_match_port(port, n, h):
     """relax_small.cu (the default for these resident integer batches) at sizes that leave a
     partial spin pair / partial 64-spin group, with and without an external field: the
