@@ -777,6 +777,19 @@ int batch_alloc(mars_batch* b) {
         } else {
             tm = relax_dense_umma_slots_per_cta();
             per_cta = static_cast<std::size_t>(2) * tm * p->np * sizeof(__half);   // S_hi + S_lo rows
+            // Persistent CTAs: when the fp16 J planes fit in L2, only as many CTAs as keep
+            // their state planes (re-read by every spin block's GEMM) in L2 beside J.  The
+            // kernel runs power-capped, so fewer CTAs also clock higher: cfg2 (N = 2000)
+            // measured 11.6K descents/s at 148 CTAs, 12.2K at 96-104 (this rule: 104), 11.1K
+            // at 64.  MARS_UMMA_GRID overrides.
+            int l2 = 0;
+            cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, p->device);
+            const std::size_t jbytes = static_cast<std::size_t>(2) * p->np * p->np * sizeof(__half);
+            int fit = p->num_sms;
+            if (l2 > 0 && jbytes < static_cast<std::size_t>(l2))
+                fit = static_cast<int>((static_cast<std::size_t>(l2) - jbytes) / per_cta);
+            fit = std::max(p->num_sms / 2, std::min(p->num_sms, fit));
+            max_grid = std::max(1, std::min(p->num_sms, env_int("MARS_UMMA_GRID", fit)));
         }
     } else {
         const char* kk = std::getenv("MARS_SPARSE_KERNEL");
