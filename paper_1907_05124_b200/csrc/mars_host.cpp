@@ -757,15 +757,16 @@ int batch_alloc(mars_batch* b) {
         tm = relax_dense_simt_slots_per_cta();
         per_cta = relax_dense_simt_work_bytes(p->np);
     } else if (p->kernel == MARS_KERNEL_DENSE_UMMA) {
-        // Small integer instances in small batches run on the on-chip warp-per-run kernel:
-        // when every run fits on the device at once (<= 16 warps x SMs) the batch is bound by
-        // its longest descent, and a warp per run walks a sweep with less latency than the
-        // 128-run tensor-core tile (cfg1, 1024 runs, N=256: 13.5K vs 12.5K descents/s).
+        // Small integer instances run on the on-chip warp-per-run kernel unless the batch
+        // fills the tensor-core kernel: a warp per run walks a sweep with less latency than
+        // the 128-run tcgen05 tile.  Measured (SK N=256 +-1, descents/s, small vs tcgen05):
+        // 1024 runs 16.0K vs 12.5K, 2368: 34.4K vs 29.1K, 4736: 69K vs 58K, 9472: 104K vs
+        // 93K, 18944: 139K vs 183K -- so up to 4 x 16 warps x SMs runs.
         // MARS_DENSE_SMALL=1 forces it (when eligible), =0 forbids it.
         const bool small_ok = !p->jlo && p->n <= relax_small_max_n();
         const int small_env = env_int("MARS_DENSE_SMALL", -1);
-        b->use_small = small_ok && (small_env == 1 ||
-                                    (small_env < 0 && b->queue_len <= static_cast<std::int64_t>(relax_small_slots_per_cta()) * p->num_sms));
+        const std::int64_t small_max_runs = static_cast<std::int64_t>(4) * relax_small_slots_per_cta() * p->num_sms;
+        b->use_small = small_ok && (small_env == 1 || (small_env < 0 && b->queue_len <= small_max_runs));
         if (b->use_small) {
             // one CTA per SM, as many warps (runs) per CTA as spread the batch over every SM:
             // the descents are latency-bound chains, so fewer warps per SM finish each sooner

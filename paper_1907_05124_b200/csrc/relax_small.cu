@@ -1,6 +1,7 @@
-// relax_small.cu -- small dense instances with integer couplings in batches small enough to be
-// resident at once (default there; MARS_DENSE_SMALL=1/0 forces it on/off).  cfg1 (1024 runs,
-// N=256): 13.5K descents/s vs 12.5K for the tensor-core kernel.
+// relax_small.cu -- small dense instances with integer couplings (N <= 256), default for
+// batches up to 4 x 16 warps x SMs runs (beyond that the tcgen05 kernel is full and faster);
+// MARS_DENSE_SMALL=1/0 forces it on/off.  cfg1 (1024 runs, N=256): 16.0K descents/s vs 12.5K
+// for the tensor-core kernel.
 //
 // Replaces, like relax_dense_umma.cu (fp32 state, same tolerance bar):
 //   mars_relax_sweep        solvers.cpp:150-161   (Gauss-Seidel in index order)
