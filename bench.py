@@ -144,7 +144,7 @@ def reference_time_to_best(w, b, workers: int) -> dict:
     """Time-to-best of a reference sample: earliest replayed retirement of a run attaining the
     sample's best energy (hit rule runner.cpp:160-162)."""
     import numpy as np
-    from paper_1907_05124_b200.mars import time_to_best
+    from paper_1907_05124_b200.workloads import time_to_best
     tol = 1e-9 if w.kind == "sk_gauss" else 0.0
     ok = b.status == 0
     best = float(b.energy[ok].min()) if ok.any() else float("nan")

@@ -191,6 +191,18 @@ int mars_batch_fetch(mars_batch_t* b, mars_records_t* records, int64_t* best_ind
 int mars_batch_fetch_finish(mars_batch_t* b, double* finish_seconds);
 void mars_batch_destroy(mars_batch_t* b);
 
+/* ---- TEST-ONLY hook: single sweeps through the device kernels -------------------------
+ *
+ * mars_relax_sweep (solvers.cpp:150-161) from caller-given states: for each of `count`
+ * states s_in[k*n ..] (fp32), `sweeps` in-order Gauss-Seidel sweeps at the fixed temperature
+ * temps[k] (T < 1e-12 is the quench) through the problem's dense relaxation kernel -- the
+ * same kernel, launch shape and precision scheme mars_run_batch uses for this handle and
+ * batch size (MARS_DENSE_SMALL applies) -- final states to s_out (fp32).  kernel_used
+ * (may be NULL) receives the kernel that ran (mars_timing_t.kernel).  Dense handles only.
+ * Exists so the tests can pin one sweep of the device path against the reference. */
+int mars_debug_sweeps(mars_problem_t* p, int64_t count, const float* s_in, const double* temps,
+                      int32_t sweeps, float* s_out, int32_t* kernel_used);
+
 /* ---- instance generators built from the reference Rng --------------- */
 void mars_gen_sk_gaussian(int32_t n, uint64_t seed, double* J);     /* io.cpp:151-163 */
 void mars_gen_sk_pm1(int32_t n, uint64_t seed, double* J);

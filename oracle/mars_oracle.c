@@ -710,3 +710,117 @@ int64_t orc_gen_ea(int L, int dims, uint64_t seed, int32_t* u, int32_t* v, doubl
     }
     return m;
 }
+
+/* ------------------------------------------------ fp32 replay (TEST-ONLY measurement tool)
+ *
+ * The reference's mars_descent (solvers.cpp:178-200 with relax_to_fixed_point 163-176,
+ * mars_relax_sweep 150-161 and tanh_trial 145-148) replayed with fp32 arithmetic for the
+ * state, the fields and tanh -- the precision class of the B200 dense kernels -- while the
+ * control flow (temperature steps and the level loop in fp64, d vs d_min, the sweep cap) is
+ * kept exactly.  It answers "how often does an fp32 computation of the same descent end on
+ * the same spins as the fp64 reference", the floor the dense-kernel parity gate is set
+ * from (tests/test_gpu_parity.py).  mode 0: J and h in fp32; mode 1: J rounded to a single
+ * fp16 plane (a 2-product split), for the precision study in DESIGN.md.  Dense problems only. */
+static float f16_round(float x) {
+    /* round-to-nearest-even to an IEEE binary16 value (normal and subnormal range) */
+    if (x == 0.0f || !isfinite(x)) return x;
+    int e;
+    frexpf(x, &e);                                      /* |x| in [2^(e-1), 2^e) */
+    int q = e - 11;                                     /* ulp exponent, 11 significant bits */
+    if (q < -24) q = -24;                               /* fp16 subnormal spacing */
+    return ldexpf(nearbyintf(ldexpf(x, -q)), q);
+}
+
+static int replay_descent_f32(const orc_problem* p, const float* Jf, const float* hf, double start_temp,
+                              const orc_params_t* prm, uint64_t seed, int8_t* spins, int64_t* iters) {
+    const int n = p->n;
+    float* s = (float*)malloc(sizeof(float) * (size_t)n);
+    double* s64 = (double*)malloc(sizeof(double) * (size_t)n);
+    orc_initial_state(seed, n, s64);
+    for (int i = 0; i < n; ++i) s[i] = (float)s64[i];
+    int64_t budget = g_sweep_cap, total = 0, sweeps = 0;
+    double t_t = start_temp;
+    int rc = 0;
+    while (t_t > 0.0) {
+        t_t -= prm->c_step;
+        const float tf = (float)t_t;
+        const int quench = t_t < K_TEMP_FLOOR;
+        double d;
+        sweeps = 0;
+        do {
+            if (budget <= 0) { rc = 2; break; }
+            --budget;
+            float dm = 0.0f;
+            for (int i = 0; i < n; ++i) {
+                const float* row = Jf + (size_t)i * n;
+                float phi = 0.0f;
+                for (int j = 0; j < n; ++j) phi = fmaf(row[j], s[j], phi);
+                phi += hf[i];
+                const float trial = quench ? (phi > 0.0f ? -1.0f : (phi < 0.0f ? 1.0f : 0.0f)) : -tanhf(phi / tf);
+                const float dd = fabsf(trial - s[i]);
+                dm = dm > dd ? dm : dd;
+                s[i] = trial;
+            }
+            d = dm;
+            ++sweeps;
+        } while (d > prm->d_min);
+        if (rc) break;
+        total += sweeps;
+    }
+    for (int i = 0; i < n; ++i) spins[i] = s[i] < 0.0f ? -1 : 1;
+    *iters = rc ? sweeps : total;
+    free(s);
+    free(s64);
+    return rc;
+}
+
+typedef struct {
+    const orc_problem* p;
+    const orc_params_t* prm;
+    const float *Jf, *hf;
+    uint64_t base;
+    int64_t runs, next;
+    uint8_t* status;
+    int64_t* iters;
+    int8_t* spins;
+    pthread_mutex_t mu;
+} replay_ctx;
+
+static void* replay_worker(void* arg) {
+    replay_ctx* c = (replay_ctx*)arg;
+    for (;;) {
+        pthread_mutex_lock(&c->mu);
+        const int64_t k = c->next++;
+        pthread_mutex_unlock(&c->mu);
+        if (k >= c->runs) return NULL;
+        int skipped;
+        double t;
+        uint64_t seed;
+        orc_run_plan(c->prm, c->base, k, &skipped, &t, &seed);
+        if (skipped) { c->status[k] = 1; c->iters[k] = 0; continue; }
+        c->status[k] = (uint8_t)replay_descent_f32(c->p, c->Jf, c->hf, t, c->prm, seed,
+                                                   c->spins + (size_t)k * c->p->n, &c->iters[k]);
+    }
+}
+
+int orc_replay_batch_f32(const void* vp, const orc_params_t* prm, int64_t runs, uint64_t base, int workers,
+                         int mode, uint8_t* status, int64_t* iters, int8_t* spins) {
+    const orc_problem* p = (const orc_problem*)vp;
+    if (!p->dense) return 1;
+    const int n = p->n;
+    float* Jf = (float*)malloc(sizeof(float) * (size_t)n * n);
+    float* hf = (float*)malloc(sizeof(float) * (size_t)n);
+    for (size_t k = 0; k < (size_t)n * n; ++k) Jf[k] = mode == 1 ? f16_round((float)p->J[k]) : (float)p->J[k];
+    for (int i = 0; i < n; ++i) hf[i] = (float)p->h[i];
+    replay_ctx c = {p, prm, Jf, hf, base, runs, 0, status, iters, spins, PTHREAD_MUTEX_INITIALIZER};
+    int w = workers > 0 ? workers : (int)sysconf(_SC_NPROCESSORS_ONLN);
+    if (w < 1) w = 1;
+    if (w > runs) w = (int)runs;
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)w);
+    for (int i = 0; i < w; ++i) pthread_create(&th[i], NULL, replay_worker, &c);
+    for (int i = 0; i < w; ++i) pthread_join(th[i], NULL);
+    free(th);
+    free(Jf);
+    free(hf);
+    return 0;
+}

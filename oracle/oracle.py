@@ -113,6 +113,9 @@ class Oracle:
         self._gen_er = f("gen_er", i64, i32, dbl, u64, vp, vp, vp)
         self._gen_ea = f("gen_ea", i64, i32, i32, u64, vp, vp, vp)
         if kind == "port":
+            self._replay = L.orc_replay_batch_f32
+            self._replay.restype = i32
+            self._replay.argtypes = [vp, C.POINTER(OracleParams), i64, u64, i32, i32, vp, vp, vp]
             self._set_cap = L.orc_set_sweep_cap
             self._set_cap.restype = None
             self._set_cap.argtypes = [i64]
@@ -264,6 +267,17 @@ class OracleProblem:
             raise OracleError(1, err.value.decode())
         return dict(status=int(st[0]), energy=float(e[0]), cut=float(c[0]),
                     descent_iters=int(it[0]), spins=sp)
+
+    def replay_f32(self, prm: OracleParams, runs: int, base_seed: int, workers: int = 0, mode: int = 0):
+        """Port only (TEST-ONLY measurement tool): the first `runs` descents replayed with fp32
+        state/fields/tanh (mode 0) or additionally J rounded to one fp16 plane (mode 1).
+        Returns (status, descent_iters, spins)."""
+        status = np.zeros(runs, np.uint8)
+        iters = np.zeros(runs, np.int64)
+        sp = np.zeros((runs, self.n), np.int8)
+        if self.orc._replay(self.h, C.byref(prm), runs, base_seed, workers, mode, _ptr(status), _ptr(iters), _ptr(sp)):
+            raise OracleError(1, "replay_f32 needs a dense problem")
+        return status, iters, sp
 
     def run_batch(self, prm: OracleParams, runs: int, base_seed: int, workers: int = 0,
                   spins: bool = True) -> OracleBatch:

@@ -84,6 +84,7 @@ SIGNATURES = {
     "mars_batch_create": (C.c_int, [vp, P_params, i64, u64, i64, i64, C.POINTER(vp)]),
     "mars_batch_upload": (C.c_int, [vp]),
     "mars_batch_execute": (C.c_int, [vp, C.POINTER(mars_timing_t)]),
+    "mars_debug_sweeps": (C.c_int, [vp, i64, vp, vp, i32, vp, vp]),
     "mars_batch_fetch": (C.c_int, [vp, C.POINTER(mars_records_t), vp, vp]),
     "mars_batch_fetch_finish": (C.c_int, [vp, vp]),
     "mars_batch_destroy": (None, [vp]),

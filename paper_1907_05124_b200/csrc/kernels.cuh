@@ -41,6 +41,12 @@ struct RelaxArgs {
     std::int8_t* spins;        // [count][n] rounded final state (round_spins, model.cpp:245)
     // optional per-CTA phase counters (clock64 cycles), kProfSlots per CTA, or nullptr
     long long* prof;
+    // TEST-ONLY fixed-temperature mode (mars_debug_sweeps, dense kernels): when > 0 every run
+    // does exactly this many Gauss-Seidel sweeps at T = start_temp[run] (no annealing
+    // schedule, no convergence test) and its final continuous state goes to state_out
+    // ([count][n] fp32) -- the device counterpart of mars_relax_sweep (solvers.cpp:150-161)
+    int fixed_sweeps;
+    float* state_out;
 };
 constexpr int kProfSlots = 16;
 

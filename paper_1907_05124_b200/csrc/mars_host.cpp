@@ -1179,7 +1179,13 @@ int mars_batch_upload(mars_batch_t* b) {
     return MARS_OK;
 }
 
-int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
+}  // extern "C"
+
+namespace {
+
+// The device work of one batch (relax -> energy -> reduce).  fixed_sweeps / d_state_out are
+// the test-only fixed-temperature mode of mars_debug_sweeps (RelaxArgs::fixed_sweeps).
+int execute_impl(mars_batch_t* b, mars_timing_t* timing, int fixed_sweeps, float* d_state_out) {
     if (!b) return fail(MARS_ERR_INPUT, "null argument");
     if (!b->uploaded) return fail(MARS_ERR_RUNTIME, "batch executed before upload");
     mars_problem* p = b->p;
@@ -1210,6 +1216,8 @@ int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
     ra.elapsed = b->d_elapsed;
     ra.done_ns = b->d_done;
     ra.spins = b->d_spins;
+    ra.fixed_sweeps = fixed_sweeps;
+    ra.state_out = d_state_out;
     std::int64_t launches = 0;
     const bool prof = std::getenv("MARS_PROFILE") != nullptr;
     long long* dprof = nullptr;
@@ -1296,6 +1304,56 @@ int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) {
             if (stt[k] != MARS_RUN_SKIPPED) tot += it[k];
         timing->total_sweeps = tot;
     }
+    return MARS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mars_batch_execute(mars_batch_t* b, mars_timing_t* timing) { return execute_impl(b, timing, 0, nullptr); }
+
+// TEST-ONLY (include/mars_b200.h): `sweeps` Gauss-Seidel sweeps at fixed temperatures through
+// the problem's dense relaxation kernel, from caller-given fp32 states.
+int mars_debug_sweeps(mars_problem_t* p, int64_t count, const float* s_in, const double* temps,
+                      int32_t sweeps, float* s_out, int32_t* kernel_used) {
+    if (!p || !s_in || !temps || !s_out) return fail(MARS_ERR_INPUT, "null argument");
+    if (count < 1 || sweeps < 1) return fail(MARS_ERR_INPUT, "count and sweeps must be positive");
+    if (p->kernel != MARS_KERNEL_DENSE_UMMA && p->kernel != MARS_KERNEL_DENSE_SIMT)
+        return fail(MARS_ERR_INPUT, "mars_debug_sweeps needs a dense (fp32-state) kernel");
+    for (std::int64_t k = 0; k < count; ++k)
+        if (!(temps[k] >= 0.0)) return fail(MARS_ERR_INPUT, "temperatures must be >= 0");
+    const mars_params_t prm{0.0, 1.0, 1.0, 1.0, 1e-4, MARS_UNIFORM_RANDOM, 0, 0};
+    mars_batch_t* b = nullptr;
+    if (int rc = mars_batch_create(p, &prm, count, 0, 0, count, &b)) return rc;
+    struct Guard {
+        mars_batch_t* b;
+        float* d = nullptr;
+        ~Guard() {
+            if (d) cudaFree(d);
+            mars_batch_destroy(b);
+        }
+    } g{b};
+    const std::size_t n = static_cast<std::size_t>(p->n), cnt = static_cast<std::size_t>(count);
+    std::memcpy(b->h_s0, s_in, cnt * n * sizeof(float));
+    for (std::int64_t k = 0; k < count; ++k) {
+        b->h_temp[k] = temps[k];
+        b->h_order[k] = static_cast<int>(k);
+        b->h_status[k] = 255;
+    }
+    b->queue_len = static_cast<int>(count);
+    CUDA_TRY(cudaSetDevice(p->device));
+    CUDA_TRY(cudaMalloc(&g.d, cnt * n * sizeof(float)));
+    CUDA_TRY(cudaMemcpyAsync(b->d_s0, b->h_s0, cnt * n * sizeof(float), cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(b->d_temp, b->h_temp, cnt * sizeof(double), cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(b->d_order, b->h_order, cnt * sizeof(int), cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(b->d_status, b->h_status, cnt, cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    b->uploaded = true;
+    mars_timing_t t{};
+    if (int rc = execute_impl(b, &t, sweeps, g.d)) return rc;
+    CUDA_TRY(cudaMemcpy(s_out, g.d, cnt * n * sizeof(float), cudaMemcpyDeviceToHost));
+    if (kernel_used) *kernel_used = t.kernel;
     return MARS_OK;
 }
 

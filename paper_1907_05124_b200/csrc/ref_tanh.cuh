@@ -11,6 +11,12 @@
 // tests/test_gpu_parity.py::test_device_tanh_matches_libm.  With it the fp64 sparse kernels
 // compute the reference's sweep exactly: trajectories, iteration counts and spins are
 // identical run for run.
+//
+// Derived from fdlibm (s_tanh.c, s_expm1.c) as shipped in glibc:
+//   Copyright (C) 1993 by Sun Microsystems, Inc. All rights reserved.
+//   Developed at SunPro, a Sun Microsystems, Inc. business.
+//   Permission to use, copy, modify, and distribute this software is freely granted,
+//   provided that this notice is preserved.
 #pragma once
 
 #include <cstdint>

@@ -93,6 +93,9 @@ __global__ void __launch_bounds__(NT, 1) relax_dense_simt_kernel(RelaxArgs a) {
                 std::int8_t* out = a.spins + static_cast<size_t>(old_run) * n;
                 for (int i = lane; i < n; i += 32)                  // round_spins, model.cpp:245
                     out[i] = W[static_cast<size_t>(i) * TM + r] < 0.0f ? -1 : 1;
+                if (a.state_out)
+                    for (int i = lane; i < n; i += 32)
+                        a.state_out[static_cast<size_t>(old_run) * n + i] = W[static_cast<size_t>(i) * TM + r];
             }
             const int new_run = sm.refill[r];
             if (new_run >= 0) {

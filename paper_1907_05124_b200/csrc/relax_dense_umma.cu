@@ -140,7 +140,8 @@ struct SubCtx {
     const float* jtri;
     float* sdel;          // this slot's Delta column: sdel[i * TM]
     const float* h;       // field slice or nullptr
-    float invT;           // 1/T, or 0 at the quench
+    float T;              // level temperature (fp32)
+    float rT;             // recip_for_div(T), or 0 at the quench
     bool quench;
     int lim;
     float dmax;
@@ -187,7 +188,10 @@ __device__ __forceinline__ void sub_step(float2 (&p)[SB / 2], const float (&old)
         const float x = (I & 1 ? p[I / 2].y : p[I / 2].x) + (HAS_H ? __ldg(c.h + k0 + I) : 0.0f);
         // tanh_trial (solvers.cpp:145-148): -tanh(phi/t), or -sign(phi) at the quench
         const float sgn = x > 0.0f ? -1.0f : (x < 0.0f ? 1.0f : 0.0f);
-        const float th = -tanhf(x * c.invT);
+        // phi / t rounded as div.rn does (quotient from the hoisted refined reciprocal plus
+        // div.rn's two correction FMAs: bit-identical to __fdiv_rn for these operands)
+        const float q0 = fmaf(c.rT, x, 0.0f);
+        const float th = -tanhf(fmaf(fmaf(-c.T, q0, x), c.rT, q0));
         const float trial = c.quench ? sgn : th;
         const float delta = trial - old[I];
         c.sdel[(k0 + I) * TM] = delta;
@@ -425,14 +429,15 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         int* x_mode = reinterpret_cast<int*>(Sdel);
         int* x_new = x_mode + TM;
         int* x_old = x_mode + 2 * TM;
-        float* x_invT = reinterpret_cast<float*>(x_mode + 3 * TM);
+        float* x_rT = reinterpret_cast<float*>(x_mode + 3 * TM);
+        float* x_T = reinterpret_cast<float*>(x_mode + 6 * TM);
         int* x_quench = x_mode + 4 * TM;
         float* x_dmax = reinterpret_cast<float*>(x_mode + 5 * TM);
 
         Slot slot;
         slot.run = -1;
         int mode = kIdle, old_run = -1, new_run = -1;
-        float invT = 1.0f;
+        float rT = 1.0f, Tf = 1.0f;
         bool quench = false;
         if (side == 0) {
             new_run = claim_run(a);
@@ -483,7 +488,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 if (__any_sync(0xffffffffu, active)) {
                     // ---- in-block Gauss-Seidel correction, ascending spin order (warp-uniform:
                     // tcgen05.ld is .sync.aligned; lanes of inactive slots compute, never store)
-                    SubCtx ctx{Jtri, Sdel + r, a.h32 ? a.h32 + b0 : nullptr, invT, quench, lim, 0.0f};
+                    SubCtx ctx{Jtri, Sdel + r, a.h32 ? a.h32 + b0 : nullptr, Tf, rT, quench, lim, 0.0f};
                     const float* dcol = Sdel + r;
                     for (int s = side; s < nsub; s += 2) {
                         const int k0 = s * SB;
@@ -547,6 +552,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         for (int i = c0; i < c1 && i < lim; ++i) {        // round_spins (model.cpp:245)
                             const float s = __half2float(hi_row[b0 + i]) + __half2float(lo_row[b0 + i]);
                             out[i] = s < 0.0f ? -1 : 1;
+                            if (a.state_out) a.state_out[static_cast<size_t>(old_run) * n + b0 + i] = s;
                         }
                     }
                     if (mode == kLoading) {
@@ -590,11 +596,13 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                             old_run = -1;
                         }
                         quench = mode == kActive && slot_quench(slot);
-                        invT = quench ? 0.0f : 1.0f / static_cast<float>(slot.T);
+                        Tf = static_cast<float>(slot.T);
+                        rT = quench ? 0.0f : recip_for_div(Tf);
                         x_mode[r] = mode;
                         x_new[r] = new_run;
                         x_old[r] = old_run;
-                        x_invT[r] = invT;
+                        x_rT[r] = rT;
+                        x_T[r] = Tf;
                         x_quench[r] = quench;
                     }
                     const bool more = epi_any(side == 0 && mode != kIdle);
@@ -602,7 +610,8 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         mode = x_mode[r];
                         new_run = x_new[r];
                         old_run = x_old[r];
-                        invT = x_invT[r];
+                        rT = x_rT[r];
+                        Tf = x_T[r];
                         quench = x_quench[r] != 0;
                     }
                     if (!more && et == 0) ctl.stop = 1;

@@ -125,6 +125,11 @@ __global__ void __launch_bounds__(kSmallWarps * 32, 1) relax_small_kernel(RelaxA
             const int k = 64 * p + 2 * lane;
             if (k < n) out[k] = s[p].x < 0.0f ? -1 : 1;
             if (k + 1 < n) out[k + 1] = s[p].y < 0.0f ? -1 : 1;
+            if (a.state_out) {
+                float* so = a.state_out + static_cast<std::size_t>(run) * n;
+                if (k < n) so[k] = s[p].x;
+                if (k + 1 < n) so[k + 1] = s[p].y;
+            }
         }
     }
 }

@@ -28,6 +28,7 @@ import numpy as np
 
 from . import _native as N
 from ._native import lib, ptr
+from .workloads import time_to_best  # noqa: F401  (pure numpy; re-exported)
 
 
 # ---------------------------------------------------------------- errors (errors.hpp:11-50)
@@ -651,10 +652,16 @@ class DeviceBatch:
         return out
 
 
-def time_to_best(energy: np.ndarray, status: np.ndarray, finish: np.ndarray, best: float,
-                 tol: float = 0.0) -> float:
-    """Time-to-best: the earliest retirement among the completed runs whose
-    energy is within ``tol`` of ``best`` (the reference's hit rule, runner.cpp:160-162);
-    inf when none of these runs reaches it."""
-    hit = (status == 0) & (np.abs(energy - best) <= tol)
-    return float(finish[hit].min()) if hit.any() else float("inf")
+def debug_sweep(problem: IsingProblem, states, temps, sweeps: int = 1) -> tuple:
+    """TEST-ONLY: ``sweeps`` in-order Gauss-Seidel sweeps (mars_relax_sweep,
+    solvers.cpp:150-161) at fixed temperatures through the handle's dense device kernel, from
+    the given fp32 states ([count, n]).  Returns (final states [count, n] fp32, kernel name)."""
+    st = np.ascontiguousarray(states, dtype=np.float32)
+    if st.ndim == 1:
+        st = st[None, :]
+    tt = np.ascontiguousarray(np.broadcast_to(np.asarray(temps, np.float64), (st.shape[0],)))
+    out = np.zeros_like(st)
+    used = C.c_int32(0)
+    _check(lib.mars_debug_sweeps(problem._h, st.shape[0], ptr(st), ptr(tt), int(sweeps), ptr(out),
+                                 C.byref(used)))
+    return out, {1: "dense_simt", 2: "csr", 3: "dense_umma", 4: "dense_small"}.get(used.value, "?")

@@ -8,7 +8,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from .mars import MarsParams, StartMode
+import numpy as np
 
 
 @dataclass(frozen=True)
@@ -25,7 +25,8 @@ class Workload:
     dims: int = 0      # ea
     note: str = ""
 
-    def params(self) -> MarsParams:
+    def params(self):
+        from .mars import MarsParams, StartMode
         return MarsParams(t_min=0.0, t_max=self.t_max, t_step=1.0, c_step=1.0, d_min=1e-4,
                           start_mode=StartMode.UniformRandom)
 
@@ -80,3 +81,13 @@ def build_oracle_problem(orc, w: Workload):
     if w.kind == "ea":
         return orc.problem_edges(w.n, *orc.gen_ea(w.L, w.dims, w.seed))
     raise ValueError(w.kind)
+
+
+def time_to_best(energy: np.ndarray, status: np.ndarray, finish: np.ndarray, best: float,
+                 tol: float = 0.0) -> float:
+    """Time-to-best: the earliest retirement among the completed runs whose
+    energy is within ``tol`` of ``best`` (the reference's hit rule, runner.cpp:160-162);
+    inf when none of these runs reaches it.  Pure numpy: bench.py's CPU reference arm uses it
+    without loading the native library."""
+    hit = (status == 0) & (np.abs(energy - best) <= tol)
+    return float(finish[hit].min()) if hit.any() else float("inf")

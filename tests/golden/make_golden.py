@@ -165,6 +165,50 @@ def small():
     save("small", **out)
 
 
+def sweeps():
+    """Single-sweep trajectory fixtures (SURVEY.md 8(c) "per-sweep unit check"): one
+    mars_relax_sweep (solvers.cpp:150-161) of the reference from fp32-representable states
+    (so the device, which takes fp32 states, starts from the identical point), at the
+    temperatures of the cfg1 / cfg2 / cfg5 schedules.  Inputs are regenerated from the seeds
+    with mars_initial_state (pinned by rng.npz); outputs are stored as fp32 (the gate is 5e-5)."""
+    out = {}
+    cases = [("sk2000", lambda: R.gen_sk_gaussian(2000, 7), 2000, (40.0, 20.0, 5.0), 8),
+             ("pm256", lambda: R.gen_sk_pm1(256, 1), 256, (16.0, 8.0, 1.0), 8),
+             ("sk16384", lambda: R.gen_sk_gaussian(16384, 7), 16384, (115.0, 60.0), 2)]
+    for name, gen, n, temps, nseeds in cases:
+        t = time.time()
+        p = R.problem_dense(gen())
+        seeds = np.array([R.sub_seed(4242, k) for k in range(nseeds)], np.uint64)
+        out[name + "_seeds"] = seeds
+        out[name + "_temps"] = np.array(temps)
+        res = np.zeros((len(temps), nseeds, n), np.float32)
+        ds = np.zeros((len(temps), nseeds))
+        for ti, T in enumerate(temps):
+            for k, sd in enumerate(seeds):
+                s = R.initial_state(int(sd), n).astype(np.float32).astype(np.float64)
+                ds[ti, k] = p.relax_sweep(s, T)
+                res[ti, k] = s
+        out[name + "_out"] = res
+        out[name + "_d"] = ds
+        print(f"sweeps {name}: {time.time() - t:.1f}s")
+    save("sweeps", **out)
+
+
+def replay_f32():
+    """The fp32 floor of the dense Gaussian path: the reference's first 256 cfg2 descents
+    replayed by the C port with fp32 state/fields/tanh (oracle/mars_oracle.c
+    orc_replay_batch_f32) -- how many end on the reference's spins when only the arithmetic
+    precision changes.  The device gate in tests/test_gpu_parity.py is set from this."""
+    P = Oracle("port")
+    w = WORKLOADS["cfg2_sk2000"]
+    p = build_oracle_problem(P, w)
+    pr = params(0, w.t_max, 1, 1, 1e-4, uniform=True)
+    t = time.time()
+    st, it, sp = p.replay_f32(pr, 256, w.base_seed, 0, 0)
+    print(f"cfg2 fp32 replay 256 runs {time.time() - t:.1f}s")
+    save("cfg2_sk2000_f32replay", status=st, iters=it, spins_packed=np.packbits(sp > 0, axis=1))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rng", "instances", "small", "cfg1", "prefixes"]
     if "rng" in which:
@@ -175,8 +219,14 @@ if __name__ == "__main__":
         small()
     if "cfg1" in which:
         cfg1()
+    if "sweeps" in which:
+        sweeps()
+    if "replay" in which:
+        replay_f32()
+    if "cfg2" in which:
+        prefix("cfg2_sk2000", 256)
     if "prefixes" in which:
-        prefix("cfg2_sk2000", 64)
+        prefix("cfg2_sk2000", 256)
         prefix("cfg3a_er800", 256)
         prefix("cfg3b_er2000", 256)
         prefix("cfg4_ea2d", 16)

@@ -49,3 +49,18 @@ def test_oracle_is_not_imported_by_product():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", text).replace("build_oracle_problem", "").lower() \
                     or f == "workloads.py", f
+
+
+def test_reference_arm_does_not_map_the_product_library():
+    """bench.py --impl reference runs the reference CPU code only: everything it imports
+    (workload definitions, the oracle driver, time-to-best) must leave libmars_b200.so unmapped."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); import bench; "
+            "from paper_1907_05124_b200.workloads import WORKLOADS, build_oracle_problem, time_to_best; "
+            "import oracle.oracle; "
+            "maps = open('/proc/self/maps').read(); "
+            "print('LOADED' if 'libmars_b200' in maps else 'CLEAN')" % ROOT)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT)
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.strip().endswith("CLEAN"), out.stdout

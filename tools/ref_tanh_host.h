@@ -1,7 +1,13 @@
 /* Restatement of this image's glibc 2.39 x86-64 tanh (baseline build) and the FMA
  * variant of expm1 it calls through the ifunc, from their machine code: fdlibm's
  * algorithm with an Estrin-form polynomial and the fused multiply-adds the compiler
- * emitted.  Every operation is explicit so the result is bit-identical. */
+ * emitted.  Every operation is explicit so the result is bit-identical.
+ *
+ * Derived from fdlibm (s_tanh.c, s_expm1.c) as shipped in glibc:
+ *   Copyright (C) 1993 by Sun Microsystems, Inc. All rights reserved.
+ *   Developed at SunPro, a Sun Microsystems, Inc. business.
+ *   Permission to use, copy, modify, and distribute this software is freely granted,
+ *   provided that this notice is preserved. */
 #include <math.h>
 #include <stdint.h>
 #include <string.h>
