@@ -92,6 +92,7 @@ struct UmmaLaunch {
 cudaError_t launch_relax_dense_umma(const RelaxArgs& a, const UmmaLaunch& u, int grid, cudaStream_t st);
 int relax_dense_umma_slots_per_cta();
 int relax_dense_umma_block();
+int relax_dense_umma_kc();      // K per pipeline stage (the TMA box width of both operand maps)
 std::size_t relax_dense_umma_plane_rows(int grid);
 
 // Level-scheduled sparse kernel (relax_csr.cu).  Spins grouped by Gauss-Seidel level,

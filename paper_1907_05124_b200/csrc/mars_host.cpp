@@ -478,8 +478,8 @@ int build_device_store(mars_problem* p) {
             if (int rc = upload(&p->dJhi, jh.data(), jh.size())) return rc;
             if (int rc = upload(&p->dJlo, jl.data(), jl.size())) return rc;
             const int tb = relax_dense_umma_block();
-            if (!make_tmap_f16_sw128(&p->tm_jhi, p->dJhi, p->np, p->np, 64, tb) ||
-                !make_tmap_f16_sw128(&p->tm_jlo, p->dJlo, p->np, p->np, 64, tb))
+            if (!make_tmap_f16(&p->tm_jhi, p->dJhi, p->np, p->np, relax_dense_umma_kc(), tb) ||
+                !make_tmap_f16(&p->tm_jlo, p->dJlo, p->np, p->np, relax_dense_umma_kc(), tb))
                 return fail(MARS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the coupling planes");
         }
     } else {
@@ -840,8 +840,8 @@ int batch_alloc(mars_batch* b) {
         b->umma.tm_jhi = p->tm_jhi;
         b->umma.tm_jlo = p->tm_jlo;
         b->umma.jlo = p->jlo;
-        if (!make_tmap_f16_sw128(&b->umma.tm_shi, b->umma.s_hi, rows, p->np, 64, tm) ||
-            !make_tmap_f16_sw128(&b->umma.tm_slo, b->umma.s_lo, rows, p->np, 64, tm))
+        if (!make_tmap_f16(&b->umma.tm_shi, b->umma.s_hi, rows, p->np, relax_dense_umma_kc(), tm) ||
+            !make_tmap_f16(&b->umma.tm_slo, b->umma.s_lo, rows, p->np, relax_dense_umma_kc(), tm))
             return fail(MARS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the state planes");
     }
     return MARS_OK;
@@ -1269,16 +1269,15 @@ int execute_impl(mars_batch_t* b, mars_timing_t* timing, int fixed_sweeps, float
                          acc[0], acc[1] / per, acc[2] / per, acc[3] / per);
         }
         const double blocks = acc[0] * (h[6] ? h[6] : 1);
-        std::fprintf(stderr,
-                     "[mars prof] grid %d: sweeps/cta %.1f, cycles/cta %.3g | per block: loads %.0f, "
-                     "wait_tmem_full %.0f, correction %.0f, writeback %.0f | producer wait ready %.0f "
-                     "empty %.0f | mma wait full %.0f tmem_empty %.0f\n",
-                     b->grid, acc[0] / b->grid, acc[1] / b->grid, acc[2] / blocks, acc[3] / blocks,
-                     acc[4] / blocks, acc[5] / blocks, acc[8] / blocks, acc[9] / blocks,
-                     acc[10] / blocks, acc[11] / blocks);
-        if (acc[13] > 0)
-            std::fprintf(stderr, "[mars prof] side-0 per walk: walk %.0f, pass0 %.0f, handoff %.0f, pass1 %.0f (%.0f walks/cta)\n",
-                         acc[12] / acc[13], acc[14] / acc[13], acc[15] / acc[13], acc[7] / acc[13], acc[13] / b->grid);
+        if (p->kernel == MARS_KERNEL_DENSE_UMMA && !b->use_small)
+            std::fprintf(stderr,
+                         "[mars prof] grid %d: sweeps/cta %.1f, cycles/cta %.3g | per block, walker: turnover %.0f, "
+                         "wait jready+tmem_full %.0f, wait fields+ld %.0f, apply %.0f, walk %.0f, store/arrive %.0f | "
+                         "helper: wait tmem_full %.0f, work %.0f, wait deltas %.0f | producer wait ready %.0f empty %.0f | "
+                         "mma wait full %.0f tmem_empty %.0f\n",
+                         b->grid, acc[0] / b->grid, acc[1] / b->grid, acc[7] / blocks, acc[2] / blocks, acc[3] / blocks,
+                         acc[4] / blocks, acc[5] / blocks, acc[12] / blocks, acc[15] / blocks, acc[14] / blocks,
+                         acc[13] / blocks, acc[8] / blocks, acc[9] / blocks, acc[10] / blocks, acc[11] / blocks);
     }
     if (timing) {
         float ms[3];

@@ -23,13 +23,23 @@
 //
 // Pipelining.  GEMM(b) consumes its K chunks starting at block b and ending with block
 // b-1, so it runs concurrently with the epilogue of block b-1 and only its last TB/KC
-// chunks wait for that epilogue's state write-back; two TMEM accumulators ping-pong.
+// chunks wait for that epilogue's state write-back (released per 64-spin half block);
+// two TMEM accumulators ping-pong.
+//
+// Epilogue (walker / helper).  The in-block walk is a serial chain per run.  A walker warp
+// walks every SB-spin sub-block of its 32 runs; before sub-block t it needs the fields
+// corrected by the Deltas of sub-blocks 0..t-1.  The helper warp of the same lane quarter
+// applies sub-blocks 0..t-2 (Delta history in TMEM, triangle rows in smem) while the walker
+// walks t-1, and writes the fields back to TMEM; the walker then applies only sub-block t-1
+// (from its registers) before walking t.  So the chain per sub-block is one 16 x 16
+// rectangle plus the 16-spin walk.  Walker <-> helper hand-offs are mbarriers (two per
+// direction per quarter, alternating, so neither side can lap the other).
 // A finished slot is refilled without stalling the pipeline: for one "loading" sweep the
 // epilogue streams the old run's final spins out and the new run's initial state in, block
 // by block, in Gauss-Seidel order, so every GEMM always reads a consistent state.
 //
 // Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer,
-// warps 2..9 = epilogue, two per TMEM lane quarter (warp w accesses lanes 32*(w%4) .. +31).
+// warps 2..5 = walkers, 6..9 = helpers (warp w accesses TMEM lanes 32*(w%4) .. +31).
 //
 // Global layout: state planes S_hi/S_lo [grid*TM][np] fp16 (row per slot, K-major for
 // UMMA), couplings J_hi/J_lo [np][np] fp16 (J symmetric, so row i of J is column i: the
@@ -52,15 +62,24 @@ using namespace umma;
 
 constexpr int TM = 128;      // runs per CTA = TMEM lanes = UMMA M
 constexpr int TB = 128;      // spins per Gauss-Seidel block = UMMA N
-constexpr int KC = 64;       // K per pipeline stage (one 128-byte swizzle atom of fp16)
+// K per pipeline stage: one 64-byte swizzle atom row of fp16.  Small stages, many of them:
+// the operand stream (state + coupling tiles from L2/HBM) is latency bound, so what sets the
+// GEMM rate is the bytes in flight -- 5 x 32 KB stages keep ~4 loads outstanding where the
+// former 2 x 64 KB ring kept ~1 (measured: the MMA waited on TMA, not on SMEM or the pipe).
+constexpr int KC = 32;
 constexpr int CPB = TB / KC; // chunks per block
-constexpr int STAGES = 2;
-constexpr int NT = 320;             // 2 control warps + 8 epilogue warps
-constexpr int EPI0 = 2;      // first epilogue warp
-constexpr int NEPI = 256;    // epilogue threads
-constexpr std::uint32_t TILE_A = TM * KC * 2;   // 16 KB
-constexpr std::uint32_t TILE_J = TB * KC * 2;   // 16 KB
+constexpr int STAGES = 5;
+constexpr int NT = 320;      // 2 control warps + 4 walker warps + 4 helper warps
+constexpr int EPI_W = 2;     // first walker warp
+constexpr int EPI_H = 6;     // first helper warp
+constexpr int NW = 128;      // walker (= helper) threads
+constexpr std::uint32_t TILE_A = TM * KC * 2;   // 8 KB
+constexpr std::uint32_t TILE_J = TB * KC * 2;   // 8 KB
 constexpr std::uint32_t STAGE_BYTES = 2 * TILE_A + 2 * TILE_J;
+// TMEM: two 128-column field accumulators (ping-pong across blocks) + the current block's
+// Delta history (one column per spin, lane = run)
+constexpr std::uint32_t TMEM_COLS = 512;
+constexpr std::uint32_t DEL_COL = 2 * TB;
 
 enum : int { kIdle = 0, kActive = 1, kLoading = 2, kDrain = 3 };
 
@@ -69,16 +88,19 @@ struct __align__(8) Ctl {
     std::uint64_t empty[STAGES];
     std::uint64_t tmem_full[2];
     std::uint64_t tmem_empty[2];
-    std::uint64_t chunk_ready;
+    std::uint64_t chunk_ready[2];   // per 64-spin half block: walker write-back done
+    std::uint64_t jready[2];        // diagonal triangle staged (per smem buffer)
+    std::uint64_t fready[4][2];     // helper -> walker: pre-corrected fields (per lane quarter)
+    std::uint64_t dready[4][2];     // walker -> helper: a sub-block's Deltas in TMEM
     std::uint64_t mma_done;
     std::uint32_t tmem_base;
     volatile std::uint32_t stop;
-    volatile std::uint32_t poison_it;
+    volatile std::uint32_t poison;  // producer stopped: the stage it arrived on carries no data
 };
 
-// dynamic smem: [stages: A_hi A_lo J_hi J_lo] [Jtri: upper triangle of the diagonal block,
+// dynamic smem: [stages: A_hi A_lo J_hi J_lo] [Jtri x 2: upper triangle of the diagonal block,
 // fp32, row i stored from column (i+1) rounded down to a multiple of 4 so every row is
-// float4-aligned] [Sdel: the block's Delta history, fp32 [TB][TM], one column per slot] [Ctl]
+// float4-aligned; double buffered so the helpers stage the next block's during this one] [Ctl]
 __host__ __device__ constexpr int tri_k0(int i) { return (i + 1) & ~3; }
 __host__ __device__ constexpr int tri_row_off(int i) {
     int off = 0;
@@ -88,11 +110,8 @@ __host__ __device__ constexpr int tri_row_off(int i) {
 constexpr std::uint32_t SMEM_STAGES = STAGES * STAGE_BYTES;
 constexpr std::uint32_t TRI = tri_row_off(TB);
 constexpr std::uint32_t SMEM_TRI = ((TRI * 4 + 127) / 128) * 128;
-constexpr std::uint32_t SMEM_SBLK = TB * TM * 4;
-constexpr std::uint32_t SMEM_TOTAL = SMEM_STAGES + SMEM_TRI + SMEM_SBLK + sizeof(Ctl);
+constexpr std::uint32_t SMEM_TOTAL = SMEM_STAGES + 2 * SMEM_TRI + sizeof(Ctl);
 static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
-
-__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
 
 __device__ __forceinline__ bool epi_any(bool v) {
     std::uint32_t r;
@@ -112,7 +131,7 @@ struct UmmaParams {
     __half* s_hi_w;
     __half* s_lo_w;
     int nb;                  // blocks per sweep = np / TB
-    int l2hint;              // coupling tiles loaded with an L2 evict_last hint (shared by all CTAs)
+    int exp;                 // EXPERIMENT knobs (MARS_UMMA_EXP): 1 = no epilogue arithmetic, 2 = no J_lo product
 };
 
 __device__ __forceinline__ void split16(float v, __half& hi, __half& lo, float& back) {
@@ -127,18 +146,15 @@ __device__ __forceinline__ int tri_row_off_rt(int i) {
     return i * TB - 4 * (2 * q * (q - 1) + q * (rem + 1));
 }
 
-// ---- the in-block Gauss-Seidel walk.  Two levels: SB-spin sub-blocks walked with a fully
-// unrolled body (fold expressions), inside a runtime loop over the block; before sub-block
-// s walks, every earlier spin's Delta (kept in this thread's smem column) is applied to its
-// fields.  Fields are fp32 pairs so the updates issue as FFMA2; J rows come from smem as
-// 16-byte loads issued before the spin's trial so their latency hides under the tanh.  The
-// compact loop keeps the hot code inside the instruction cache (a fully unrolled 128-spin
-// triangle is ~220 KB of SASS, streamed from L2 by every SM).
+// ---- the in-block Gauss-Seidel walk of one SB-spin sub-block (one thread = one run), fully
+// unrolled with fold expressions.  Fields are fp32 pairs so the in-sub-block updates issue as
+// FFMA2; the J rows (diagonal block's upper triangle in smem) are 16-byte loads issued before
+// the spin's trial so their latency hides under the tanh.  Each spin's change Delta is kept
+// in a register (del[I]) -- the walker stores the sub-block's Deltas to TMEM for the helper.
 constexpr int SB = 16;
 
 struct SubCtx {
     const float* jtri;
-    float* sdel;          // this slot's Delta column: sdel[i * TM]
     const float* h;       // field slice or nullptr
     float T;              // level temperature (fp32)
     float rT;             // recip_for_div(T), or 0 at the quench
@@ -149,6 +165,11 @@ struct SubCtx {
 
 __device__ __forceinline__ float2 ffma2(float2 a, float b, float2 c) {
     return __ffma2_rn(a, make_float2(b, b), c);
+}
+
+// address of J[i][k0 + m], m >= tri_k0(i) - k0, inside the packed triangle
+__device__ __forceinline__ const float* tri_ptr(const float* jtri, int i, int col) {
+    return jtri + tri_row_off_rt(i) - tri_k0(i) + col;
 }
 
 template <int I, int G>
@@ -174,49 +195,65 @@ __device__ __forceinline__ void sub_update(float2 (&p)[SB / 2], const float4 (&j
 }
 
 template <int I, bool FULL, bool HAS_H>
-__device__ __forceinline__ void sub_step(float2 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB], int k0,
-                                         SubCtx& c) {
+__device__ __forceinline__ void sub_step(float2 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB],
+                                         float (&del)[SB], int k0, SubCtx& c) {
     if (FULL || k0 + I < c.lim) {
         // J[k0+I][k0 + 4g ..] for the groups this spin updates, issued before the trial
         float4 jr[SB / 4];
         if constexpr (I + 1 < SB) {
-            const int i = k0 + I;
-            const float* row = c.jtri + tri_row_off_rt(i) - tri_k0(i) + k0;   // row[m] = J[i][k0+m]
+            const float* row = tri_ptr(c.jtri, k0 + I, k0);   // row[m] = J[k0+I][k0+m]
 #pragma unroll
             for (int g = ((I + 1) & ~3) / 4; g < SB / 4; ++g) jr[g] = *reinterpret_cast<const float4*>(row + 4 * g);
         }
         const float x = (I & 1 ? p[I / 2].y : p[I / 2].x) + (HAS_H ? __ldg(c.h + k0 + I) : 0.0f);
-        // tanh_trial (solvers.cpp:145-148): -tanh(phi/t), or -sign(phi) at the quench
+        // tanh_trial (solvers.cpp:145-148): -tanh(phi/t), or -sign(phi) at the quench; phi / t
+        // rounded as div.rn does (quotient from the hoisted refined reciprocal plus div.rn's
+        // two correction FMAs: bit-identical to __fdiv_rn for these operands)
         const float sgn = x > 0.0f ? -1.0f : (x < 0.0f ? 1.0f : 0.0f);
-        // phi / t rounded as div.rn does (quotient from the hoisted refined reciprocal plus
-        // div.rn's two correction FMAs: bit-identical to __fdiv_rn for these operands)
         const float q0 = fmaf(c.rT, x, 0.0f);
         const float th = -tanhf(fmaf(fmaf(-c.T, q0, x), c.rT, q0));
         const float trial = c.quench ? sgn : th;
         const float delta = trial - old[I];
-        c.sdel[(k0 + I) * TM] = delta;
+        del[I] = delta;
         nv[I] = trial;
         c.dmax = fmaxf(c.dmax, fabsf(delta));
         if constexpr (I + 1 < SB)
             sub_update<I>(p, jr, delta, std::make_integer_sequence<int, SB / 4 - ((I + 1) & ~3) / 4>{});
     } else {
         nv[I] = old[I];
+        del[I] = 0.0f;
     }
 }
 
 template <bool FULL, bool HAS_H, int... I>
-__device__ __forceinline__ void sub_walk(float2 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB], int k0,
-                                         SubCtx& c, std::integer_sequence<int, I...>) {
-    (sub_step<I, FULL, HAS_H>(p, old, nv, k0, c), ...);
+__device__ __forceinline__ void sub_walk(float2 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB],
+                                         float (&del)[SB], int k0, SubCtx& c, std::integer_sequence<int, I...>) {
+    (sub_step<I, FULL, HAS_H>(p, old, nv, del, k0, c), ...);
 }
 
 template <bool HAS_H>
 __device__ __forceinline__ void walk_dispatch(float2 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB],
-                                              int k0, SubCtx& c) {
+                                              float (&del)[SB], int k0, SubCtx& c) {
     if (k0 + SB <= c.lim)
-        sub_walk<true, HAS_H>(p, old, nv, k0, c, std::make_integer_sequence<int, SB>{});
+        sub_walk<true, HAS_H>(p, old, nv, del, k0, c, std::make_integer_sequence<int, SB>{});
     else
-        sub_walk<false, HAS_H>(p, old, nv, k0, c, std::make_integer_sequence<int, SB>{});
+        sub_walk<false, HAS_H>(p, old, nv, del, k0, c, std::make_integer_sequence<int, SB>{});
+}
+
+// fields (fp32 pairs) += J[j0 .. j0+16)[col .. col+16)^T * d[0..16): the 16 x 16 rectangle
+// coupling one sub-block's Deltas to a later sub-block's fields (rows from the triangle)
+__device__ __forceinline__ void apply_rect16(float2 (&pf)[SB / 2], const float* jtri, int j0, int col,
+                                             const float (&d)[SB]) {
+#pragma unroll
+    for (int j = 0; j < SB; ++j) {
+        const float4* jr = reinterpret_cast<const float4*>(tri_ptr(jtri, j0 + j, col));
+#pragma unroll
+        for (int m = 0; m < SB / 4; ++m) {
+            const float4 jv = jr[m];
+            pf[2 * m] = ffma2(make_float2(jv.x, jv.y), d[j], pf[2 * m]);
+            pf[2 * m + 1] = ffma2(make_float2(jv.z, jv.w), d[j], pf[2 * m + 1]);
+        }
+    }
 }
 
 __device__ __forceinline__ void tmem_ld16(std::uint32_t taddr, float (&v)[16]) {
@@ -233,13 +270,29 @@ __device__ __forceinline__ void tmem_ld16(std::uint32_t taddr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ void load_old16(const __half* hi, const __half* lo, float (&old)[SB]) {
+__device__ __forceinline__ void tmem_st16f(std::uint32_t taddr, const float (&v)[16]) {
+    std::uint32_t r[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(v[i]);
+    tmem_st16(taddr, r);
+}
+
+struct Old16 {
+    uint4 h[2], l[2];
+};
+
+__device__ __forceinline__ void fetch_old16(const __half* hi, const __half* lo, Old16& o) {
+    o.h[0] = *reinterpret_cast<const uint4*>(hi);
+    o.h[1] = *reinterpret_cast<const uint4*>(hi + 8);
+    o.l[0] = *reinterpret_cast<const uint4*>(lo);
+    o.l[1] = *reinterpret_cast<const uint4*>(lo + 8);
+}
+
+__device__ __forceinline__ void unpack_old16(const Old16& o, float (&old)[SB]) {
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
-        const uint4 hv = *reinterpret_cast<const uint4*>(hi + v * 8);
-        const uint4 lv = *reinterpret_cast<const uint4*>(lo + v * 8);
-        const __half* h8 = reinterpret_cast<const __half*>(&hv);
-        const __half* l8 = reinterpret_cast<const __half*>(&lv);
+        const __half* h8 = reinterpret_cast<const __half*>(&o.h[v]);
+        const __half* l8 = reinterpret_cast<const __half*>(&o.l[v]);
 #pragma unroll
         for (int e = 0; e < 8; ++e) old[v * 8 + e] = __half2float(h8[e]) + __half2float(l8[e]);
     }
@@ -267,6 +320,20 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
+// arrive on `bar` once every cp.async this thread issued so far has landed (no pending-count
+// increment: the barrier's expected count includes this arrival)
+__device__ __forceinline__ void cp_async_arrive_noinc(std::uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// the diagonal block's upper triangle (fp32) -> packed smem layout, cooperative over the
+// helper warps (128 threads)
+__device__ __forceinline__ void issue_jtri(float* dst, const float* J32, int np, int b0, int ht) {
+    for (int f = ht; f < TB * TB / 4; f += TM) {
+        const int i = f / (TB / 4), k = (f % (TB / 4)) * 4;
+        if (k >= tri_k0(i)) cp_async16(dst + tri_row_off_rt(i) + k - tri_k0(i), J32 + static_cast<size_t>(b0 + i) * np + b0 + k);
+    }
+}
 
 template <bool JLO>
 __global__ void __launch_bounds__(NT, 1)
@@ -277,9 +344,8 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* base = smem_raw;   // SWIZZLE_128B tiles need 1024-byte alignment (checked)
     if (threadIdx.x == 0 && (smem_u32(smem_raw) & 1023u) != 0) __trap();
-    float* Jtri = reinterpret_cast<float*>(base + SMEM_STAGES);
-    float* Sdel = reinterpret_cast<float*>(base + SMEM_STAGES + SMEM_TRI);
-    Ctl& ctl = *reinterpret_cast<Ctl*>(base + SMEM_STAGES + SMEM_TRI + SMEM_SBLK);
+    float* Jtri0 = reinterpret_cast<float*>(base + SMEM_STAGES);
+    Ctl& ctl = *reinterpret_cast<Ctl*>(base + SMEM_STAGES + 2 * SMEM_TRI);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int np = a.np, n = a.n, nb = up.nb, nk = np / KC;
@@ -292,15 +358,21 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&ctl.tmem_full[s], 1);
-            mbar_init(&ctl.tmem_empty[s], NEPI);
+            mbar_init(&ctl.tmem_empty[s], NW);
+            mbar_init(&ctl.chunk_ready[s], NW);
+            mbar_init(&ctl.jready[s], NW);
         }
-        mbar_init(&ctl.chunk_ready, NEPI);
+        for (int q = 0; q < 4; ++q)
+            for (int s = 0; s < 2; ++s) {
+                mbar_init(&ctl.fready[q][s], 32);
+                mbar_init(&ctl.dready[q][s], 32);
+            }
         mbar_init(&ctl.mma_done, 1);
         ctl.stop = 0;
-        ctl.poison_it = 0xFFFFFFFFu;
+        ctl.poison = 0;
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc(&ctl.tmem_base, 2 * TB);
+    if (warp == 1) tmem_alloc(&ctl.tmem_base, TMEM_COLS);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -308,151 +380,142 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
 
     if (warp == 0) {
         // ================================================================ TMA producer
+        // Whole warp converged; one elected lane issues.  Stage / phase / chunk advance
+        // incrementally (no division in the loop).
         if (lane == 0) {
             tma_prefetch_desc(&tm_shi);
             tma_prefetch_desc(&tm_slo);
             tma_prefetch_desc(&tm_jhi);
             if (JLO) tma_prefetch_desc(&tm_jlo);
-            const std::uint64_t jpol = policy_evict_last();
-            std::uint32_t g = 0, it = 0;
-            long long w_ready = 0, w_empty = 0;
-            for (;;) {
-                for (int b = 0; b < nb; ++b, ++g) {
-                    for (int j = 0; j < nk; ++j, ++it) {
-                        if (j == nk - CPB && g > 0) {
-                            // the last chunks of GEMM(b) are block b-1: wait for its update
-                            const long long t0 = clock64();
-                            mbar_wait(&ctl.chunk_ready, (g - 1) & 1);
-                            w_ready += clock64() - t0;
-                            if (ctl.stop) {
-                                const int s = it % STAGES;
-                                mbar_wait(&ctl.empty[s], ((it / STAGES) & 1) ^ 1);
-                                ctl.poison_it = it;
+        }
+        __syncwarp();
+        const std::uint64_t jpol = policy_evict_last();
+        const std::uint32_t smem0 = smem_u32(base);
+        const std::uint32_t full0 = smem_u32(&ctl.full[0]);
+        const std::uint32_t tx = JLO ? STAGE_BYTES : STAGE_BYTES - TILE_J;
+        std::uint32_t g = 0, s = 0, ph = 0;
+        long long w_ready = 0, w_empty = 0;
+        for (;;) {
+            for (int b = 0; b < nb; ++b, ++g) {
+                int c = b * CPB;                               // chunk order: block b first
+                for (int j = 0; j < nk; ++j) {
+                    if ((j == nk - CPB || j == nk - CPB / 2) && g > 0) {
+                        // the last chunks of GEMM(b) are block b-1: wait for the walker's
+                        // write-back of that half block (one barrier per 64-spin half)
+                        const int half = j == nk - CPB ? 0 : 1;
+                        const long long t0 = clock64();
+                        mbar_wait(&ctl.chunk_ready[half], (g - 1) & 1);
+                        w_ready += clock64() - t0;
+                        if (half == 1 && ctl.stop) {
+                            mbar_wait(&ctl.empty[s], ph ^ 1);
+                            if (lane == 0) {
+                                ctl.poison = 1;
                                 mbar_arrive(&ctl.full[s]);
                                 if (a.prof) {
                                     a.prof[blockIdx.x * kProfSlots + 8] = w_ready;
                                     a.prof[blockIdx.x * kProfSlots + 9] = w_empty;
                                 }
-                                goto producer_done;
                             }
+                            goto producer_done;
                         }
-                        const int s = it % STAGES;
-                        const int c = (b * CPB + j) % nk;
-                        const long long t1 = clock64();
-                        mbar_wait(&ctl.empty[s], ((it / STAGES) & 1) ^ 1);
-                        w_empty += clock64() - t1;
-                        unsigned char* st = base + s * STAGE_BYTES;
-                        mbar_arrive_expect_tx(&ctl.full[s], JLO ? STAGE_BYTES : STAGE_BYTES - TILE_J);
-                        tma_load_2d(st, &tm_shi, &ctl.full[s], c * KC, row0);
-                        tma_load_2d(st + TILE_A, &tm_slo, &ctl.full[s], c * KC, row0);
-                        // the coupling tiles are read by every CTA every sweep: keep them in L2
-                        // ahead of the per-CTA state planes (155 MB at 148 CTAs > L2)
-                        if (up.l2hint) {
-                            tma_load_2d_hint(st + 2 * TILE_A, &tm_jhi, &ctl.full[s], c * KC, b * TB, jpol);
-                            if (JLO) tma_load_2d_hint(st + 2 * TILE_A + TILE_J, &tm_jlo, &ctl.full[s], c * KC, b * TB, jpol);
-                        } else {
-                            tma_load_2d(st + 2 * TILE_A, &tm_jhi, &ctl.full[s], c * KC, b * TB);
-                            if (JLO) tma_load_2d(st + 2 * TILE_A + TILE_J, &tm_jlo, &ctl.full[s], c * KC, b * TB);
-                        }
+                    }
+                    const long long t1 = clock64();
+                    mbar_wait(&ctl.empty[s], ph ^ 1);
+                    w_empty += clock64() - t1;
+                    const std::uint32_t st = smem0 + s * STAGE_BYTES;
+                    const std::uint32_t fb = full0 + s * 8;
+                    mbar_arrive_expect_tx_elect(&ctl.full[s], tx);
+                    tma_load_2d_elect(st, &tm_shi, fb, c * KC, row0);
+                    tma_load_2d_elect(st + TILE_A, &tm_slo, fb, c * KC, row0);
+                    // the coupling tiles are read by every CTA every sweep: keep them in L2
+                    // ahead of the per-CTA state planes
+                    tma_load_2d_hint_elect(st + 2 * TILE_A, &tm_jhi, fb, c * KC, b * TB, jpol);
+                    if (JLO) tma_load_2d_hint_elect(st + 2 * TILE_A + TILE_J, &tm_jlo, fb, c * KC, b * TB, jpol);
+                    if (++c == nk) c = 0;
+                    if (++s == STAGES) {
+                        s = 0;
+                        ph ^= 1;
                     }
                 }
             }
-        producer_done:;
         }
+    producer_done:;
     } else if (warp == 1) {
         // ================================================================ MMA issuer
-        if (lane == 0) {
-            constexpr std::uint32_t idesc = idesc_f16(TM, TB, 0);
-            std::uint32_t g = 0, it = 0;
-            long long w_full = 0, w_tmem = 0;
-            for (;;) {
-                for (int b = 0; b < nb; ++b, ++g) {
-                    const int buf = g & 1;
-                    const long long t0 = clock64();
-                    mbar_wait(&ctl.tmem_empty[buf], ((g >> 1) & 1) ^ 1);
-                    w_tmem += clock64() - t0;
-                    tc_fence_after();
-                    const std::uint32_t d = tmem + buf * TB;
-                    for (int j = 0; j < nk; ++j, ++it) {
-                        const int s = it % STAGES;
-                        const long long t1 = clock64();
-                        mbar_wait(&ctl.full[s], (it / STAGES) & 1);
-                        w_full += clock64() - t1;
-                        if (ctl.poison_it == it) {
-                            if (a.prof) {
-                                a.prof[blockIdx.x * kProfSlots + 10] = w_full;
-                                a.prof[blockIdx.x * kProfSlots + 11] = w_tmem;
-                            }
-                            goto mma_done;
+        // Whole warp converged (descriptors are warp-uniform: uniform registers); one
+        // elected lane issues each tcgen05.mma / commit.
+        constexpr std::uint32_t idesc = idesc_f16(TM, TB, 0);
+        const std::uint32_t smem0 = smem_u32(base);
+        std::uint32_t g = 0, s = 0, ph = 0;
+        long long w_full = 0, w_tmem = 0;
+        for (;;) {
+            for (int b = 0; b < nb; ++b, ++g) {
+                const int buf = g & 1;
+                const long long t0 = clock64();
+                mbar_wait(&ctl.tmem_empty[buf], ((g >> 1) & 1) ^ 1);
+                w_tmem += clock64() - t0;
+                tc_fence_after();
+                const std::uint32_t d = tmem + buf * TB;
+                for (int j = 0; j < nk; ++j) {
+                    const long long t1 = clock64();
+                    mbar_wait(&ctl.full[s], ph);
+                    w_full += clock64() - t1;
+                    // the producer can only stop at the second write-back wait of a block
+                    if (j == nk - CPB / 2 && ctl.poison) {
+                        if (a.prof && lane == 0) {
+                            a.prof[blockIdx.x * kProfSlots + 10] = w_full;
+                            a.prof[blockIdx.x * kProfSlots + 11] = w_tmem;
                         }
-                        tc_fence_after();
-                        const std::uint32_t st = smem_u32(base + s * STAGE_BYTES);
-#pragma unroll
-                        for (int kk = 0; kk < KC / 16; ++kk) {
-                            const std::uint64_t ahi = desc_k_sw128(st + kk * 32);
-                            const std::uint64_t alo = desc_k_sw128(st + TILE_A + kk * 32);
-                            const std::uint64_t jhi = desc_k_sw128(st + 2 * TILE_A + kk * 32);
-                            mma_f16_ss(d, ahi, jhi, idesc, (j | kk) != 0);
-                            mma_f16_ss(d, alo, jhi, idesc, 1);
-                            if (JLO) {
-                                const std::uint64_t jlo = desc_k_sw128(st + 2 * TILE_A + TILE_J + kk * 32);
-                                mma_f16_ss(d, ahi, jlo, idesc, 1);
-                            }
-                        }
-                        mma_commit(&ctl.empty[s]);
+                        goto mma_done;
                     }
-                    mma_commit(&ctl.tmem_full[buf]);
+                    tc_fence_after();
+                    const std::uint32_t st = smem0 + s * STAGE_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < KC / 16; ++kk) {
+                        const std::uint64_t ahi = desc_k_sw64(st + kk * 32);
+                        const std::uint64_t alo = desc_k_sw64(st + TILE_A + kk * 32);
+                        const std::uint64_t jhi = desc_k_sw64(st + 2 * TILE_A + kk * 32);
+                        mma_f16_ss_elect(d, ahi, jhi, idesc, (j | kk) != 0);
+                        mma_f16_ss_elect(d, alo, jhi, idesc, 1);
+                        if (JLO && !(up.exp & 2)) {
+                            const std::uint64_t jlo = desc_k_sw64(st + 2 * TILE_A + TILE_J + kk * 32);
+                            mma_f16_ss_elect(d, ahi, jlo, idesc, 1);
+                        }
+                    }
+                    mma_commit_elect(&ctl.empty[s]);
+                    if (++s == STAGES) {
+                        s = 0;
+                        ph ^= 1;
+                    }
                 }
+                mma_commit_elect(&ctl.tmem_full[buf]);
             }
-        mma_done:
-            mma_commit(&ctl.mma_done);
-            mbar_wait(&ctl.mma_done, 0);
         }
+    mma_done:
+        mma_commit_elect(&ctl.mma_done);
+        mbar_wait(&ctl.mma_done, 0);
         __syncwarp();
-    } else {
-        // ================================================================ epilogue
-        // Eight warps, two per TMEM lane quarter: warp pair (w, w+4) owns slots
-        // r = 32*(w%4) + lane and alternates the SB-spin sub-blocks of every block, so one warp
-        // pre-applies the Delta history to its next sub-block while its partner walks the
-        // current one; a pair-private named barrier hands each finished sub-block's Delta over.
-        // Side 0 owns the slot state machine and publishes it to side 1 at sweep ends.
-        const int q = warp & 3;                            // TMEM lane quarter
-        const int side = warp >= EPI0 + 4 ? 1 : 0;
-        const int r = q * 32 + lane;                       // slot = TMEM lane
-        const int et = threadIdx.x - EPI0 * 32;            // 0..255 for cooperative loads
-        // hand-off of sub-block h uses named barrier 2 + 2q + (h & 1): two IDs per pair, so a
-        // producer running ahead can never complete the phase its partner has not reached
-        const int pair_bar = 2 + 2 * q;
+    } else if (warp < EPI_H) {
+        // ================================================================ walkers (W)
+        // Warp w owns the runs of TMEM lane quarter q = w % 4 (slot r = 32q + lane) and walks
+        // every sub-block of every block in ascending spin order.  Before walking sub-block t
+        // it takes the fields the helper pre-corrected (GEMM + Deltas of sub-blocks < t-1,
+        // written back to TMEM) and applies the previous sub-block's Deltas from its own
+        // registers, so the serial chain per sub-block is one 16 x 16 rectangle + the walk.
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        const int wt = threadIdx.x - EPI_W * 32;           // 0..127
+        const std::uint32_t lane_t = static_cast<std::uint32_t>(q * 32) << 16;
         __half* hi_row = up.s_hi_w + static_cast<size_t>(row0 + r) * np;
         __half* lo_row = up.s_lo_w + static_cast<size_t>(row0 + r) * np;
-        // sweep-boundary exchange area (the Delta history is dead between blocks)
-        int* x_mode = reinterpret_cast<int*>(Sdel);
-        int* x_new = x_mode + TM;
-        int* x_old = x_mode + 2 * TM;
-        float* x_rT = reinterpret_cast<float*>(x_mode + 3 * TM);
-        float* x_T = reinterpret_cast<float*>(x_mode + 6 * TM);
-        int* x_quench = x_mode + 4 * TM;
-        float* x_dmax = reinterpret_cast<float*>(x_mode + 5 * TM);
-
         Slot slot;
         slot.run = -1;
-        int mode = kIdle, old_run = -1, new_run = -1;
+        int new_run = claim_run(a);
+        int mode = new_run >= 0 ? kLoading : kIdle, old_run = -1;
         float rT = 1.0f, Tf = 1.0f;
         bool quench = false;
-        if (side == 0) {
-            new_run = claim_run(a);
-            mode = new_run >= 0 ? kLoading : kIdle;
-            x_mode[r] = mode;
-            x_new[r] = new_run;
-        }
-        epi_sync();
-        if (side == 1) {
-            mode = x_mode[r];
-            new_run = x_new[r];
-        }
-        std::uint32_t g = 0;
-        long long c_loads = 0, c_wait = 0, c_corr = 0, c_wb = 0, n_sweeps = 0;
-        long long c_walk = 0, c_pass0 = 0, c_hand = 0, c_pass1 = 0, n_walks = 0;
+        std::uint32_t g = 0, fe = 0, de = 0;                // block, F-event and D-event counters
+        long long c_wait = 0, c_f = 0, c_apply = 0, c_walk = 0, c_turn = 0, c_st = 0, n_sweeps = 0;
         const long long c_start = clock64();
 
         for (;;) {
@@ -463,93 +526,15 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 const int b0 = b * TB;
                 const int lim = min(TB, n - b0);
                 const int nsub = (lim + SB - 1) / SB;
-                long long t0 = clock64();
-                // diagonal block's upper triangle -> smem, overlapping the wait for GEMM(b)
-                epi_sync();
-                for (int f = et; f < TB * TB / 4; f += 2 * TM) {
-                    const int i = f / (TB / 4), k = (f % (TB / 4)) * 4;
-                    if (k >= tri_k0(i))
-                        cp_async16(Jtri + tri_row_off_rt(i) + k - tri_k0(i),
-                                   a.J32 + static_cast<size_t>(b0 + i) * np + b0 + k);
-                }
+                const float* jtri = Jtri0 + (g & 1) * (SMEM_TRI / 4);
                 const int buf = g & 1;
-                long long t1 = clock64();
-                mbar_wait(&ctl.tmem_full[buf], (g >> 1) & 1);
-                long long t2 = clock64();
-                c_wait += t2 - t1;
-                cp_async_wait_all();
-                epi_sync();
-                const long long t2b = clock64();
-                c_loads += (t1 - t0) + (t2b - t2);
-                t2 = t2b;
-                tc_fence_after();
-                const std::uint32_t tacc = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + buf * TB;
-
-                if (__any_sync(0xffffffffu, active)) {
-                    // ---- in-block Gauss-Seidel correction, ascending spin order (warp-uniform:
-                    // tcgen05.ld is .sync.aligned; lanes of inactive slots compute, never store)
-                    SubCtx ctx{Jtri, Sdel + r, a.h32 ? a.h32 + b0 : nullptr, Tf, rT, quench, lim, 0.0f};
-                    const float* dcol = Sdel + r;
-                    for (int s = side; s < nsub; s += 2) {
-                        const int k0 = s * SB;
-                        float old[SB];
-                        load_old16(hi_row + b0 + k0, lo_row + b0 + k0, old);
-                        float pv[SB];
-                        tmem_ld16(tacc + k0, pv);
-                        float2 pf[SB / 2];
-#pragma unroll
-                        for (int j = 0; j < SB / 2; ++j) pf[j] = make_float2(pv[2 * j], pv[2 * j + 1]);
-                        // corrections J[j][k0..k0+SB) * Delta_j: first every Delta already final
-                        // (sub-blocks < s-1), then -- after the partner hands it over -- s-1's
-                        const int jpre = s > 0 ? k0 - SB : 0;
-                        long long tp = clock64();
-                        for (int pass = 0; pass < 2; ++pass) {
-                            const int jb = pass == 0 ? 0 : jpre, je = pass == 0 ? jpre : k0;
-                            if (pass == 1) {
-                                if (s == 0) break;
-                                const long long ta = clock64();
-                                c_pass0 += ta - tp;
-                                asm volatile("bar.sync %0, 64;\n" ::"r"(pair_bar + ((s - 1) & 1)) : "memory");
-                                tp = clock64();
-                                c_hand += tp - ta;
-                            }
-#pragma unroll 2
-                            for (int j = jb; j < je; ++j) {
-                                const float d = dcol[j * TM];
-                                const float4* jr = reinterpret_cast<const float4*>(
-                                    Jtri + tri_row_off_rt(j) + k0 - tri_k0(j));
-#pragma unroll
-                                for (int m = 0; m < SB / 4; ++m) {
-                                    const float4 jv = jr[m];
-                                    pf[2 * m] = ffma2(make_float2(jv.x, jv.y), d, pf[2 * m]);
-                                    pf[2 * m + 1] = ffma2(make_float2(jv.z, jv.w), d, pf[2 * m + 1]);
-                                }
-                            }
-                        }
-                        float nv[SB];
-                        const long long tw = clock64();
-                        if (s > 0) c_pass1 += tw - tp; else c_pass0 += tw - tp;
-                        if (ctx.h) walk_dispatch<true>(pf, old, nv, k0, ctx);
-                        else walk_dispatch<false>(pf, old, nv, k0, ctx);
-                        c_walk += clock64() - tw;
-                        ++n_walks;
-                        if (active) store_new16(hi_row + b0 + k0, lo_row + b0 + k0, nv);
-                        if (s + 1 < nsub) asm volatile("bar.arrive %0, 64;\n" ::"r"(pair_bar + (s & 1)) : "memory");
-                    }
-                    dmax = fmaxf(dmax, ctx.dmax);
-                }
-                tc_fence_before();
-                mbar_arrive(&ctl.tmem_empty[buf]);
-                const long long t3 = clock64();
-                c_corr += t3 - t2;
-                t2 = t3;
+                long long t0 = clock64();
                 if (!active && (mode == kLoading || mode == kDrain)) {
-                    // ---- slot turnover, block by block (each side one half of the columns):
-                    // the old run's rounded spins out, the new run's initial state in
-                    const int c0 = side * (TB / 2), c1 = c0 + TB / 2;
+                    // ---- slot turnover, block by block: the old run's rounded spins out, the
+                    // new run's initial state in (before this block's chunks are re-read)
                     if (old_run >= 0) {
                         std::int8_t* out = a.spins + static_cast<size_t>(old_run) * n + b0;
-                        for (int i = c0; i < c1 && i < lim; ++i) {        // round_spins (model.cpp:245)
+                        for (int i = 0; i < lim; ++i) {                 // round_spins (model.cpp:245)
                             const float s = __half2float(hi_row[b0 + i]) + __half2float(lo_row[b0 + i]);
                             out[i] = s < 0.0f ? -1 : 1;
                             if (a.state_out) a.state_out[static_cast<size_t>(old_run) * n + b0 + i] = s;
@@ -557,7 +542,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     }
                     if (mode == kLoading) {
                         const float* src = a.s0 + static_cast<size_t>(new_run) * n + b0;
-                        for (int v = c0 / 8; v < c1 / 8; ++v) {
+                        for (int v = 0; v < TB / 8; ++v) {
                             uint4 hv, lv;
                             __half* h8 = reinterpret_cast<__half*>(&hv);
                             __half* l8 = reinterpret_cast<__half*>(&lv);
@@ -571,91 +556,222 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         }
                     }
                 }
-                c_wb += clock64() - t2;
+                long long t1 = clock64();
+                c_turn += t1 - t0;
+                Old16 pre;
+                fetch_old16(hi_row + b0, lo_row + b0, pre);
+                mbar_wait(&ctl.jready[buf], (g >> 1) & 1);
+                mbar_wait(&ctl.tmem_full[buf], (g >> 1) & 1);
+                tc_fence_after();
+                t0 = clock64();
+                c_wait += t0 - t1;
+                const std::uint32_t tacc = tmem + lane_t + buf * TB;
+                SubCtx ctx{jtri, a.h32 ? a.h32 + b0 : nullptr, Tf, rT, quench, lim, 0.0f};
+                float prev[SB];                                 // Deltas of sub-block t-1
+                for (int t = 0; t < nsub; ++t) {
+                    const int k0 = t * SB;
+                    float old[SB];
+                    unpack_old16(pre, old);
+                    if (t + 1 < nsub) fetch_old16(hi_row + b0 + k0 + SB, lo_row + b0 + k0 + SB, pre);
+                    t1 = clock64();
+                    if (t >= 2) {
+                        mbar_wait(&ctl.fready[q][fe & 1], (fe >> 1) & 1);
+                        ++fe;
+                        tc_fence_after();
+                    }
+                    float pv[SB];
+                    tmem_ld16(tacc + k0, pv);
+                    float2 pf[SB / 2];
+#pragma unroll
+                    for (int j = 0; j < SB / 2; ++j) pf[j] = make_float2(pv[2 * j], pv[2 * j + 1]);
+                    t0 = clock64();
+                    c_f += t0 - t1;
+                    if (t >= 1 && !(up.exp & 1)) apply_rect16(pf, jtri, k0 - SB, k0, prev);
+                    t1 = clock64();
+                    c_apply += t1 - t0;
+                    float nv[SB];
+                    if (up.exp & 1) {
+#pragma unroll
+                        for (int j = 0; j < SB; ++j) { nv[j] = old[j]; prev[j] = 0.0f; }
+                        ctx.dmax = fmaxf(ctx.dmax, pf[0].x * 1e-30f);
+                    } else if (ctx.h) walk_dispatch<true>(pf, old, nv, prev, k0, ctx);
+                    else walk_dispatch<false>(pf, old, nv, prev, k0, ctx);
+                    t0 = clock64();
+                    c_walk += t0 - t1;
+                    if (active) store_new16(hi_row + b0 + k0, lo_row + b0 + k0, nv);
+                    if (t == 0 || t + 2 < nsub) {
+                        // the helper needs this sub-block's Deltas (for sub-blocks >= t + 2)
+                        tmem_st16f(tmem + lane_t + DEL_COL + k0, prev);
+                        tmem_st_wait();
+                        tc_fence_before();
+                        mbar_arrive(&ctl.dready[q][de & 1]);
+                        ++de;
+                    }
+                    if (t == min(TB / 2 / SB, nsub) - 1) {
+                        // first 64-spin chunk of this block written back: its GEMM chunk may go
+                        fence_proxy_async_global();
+                        mbar_arrive(&ctl.chunk_ready[0]);
+                    }
+                    c_st += clock64() - t0;
+                }
+                dmax = fmaxf(dmax, ctx.dmax);
+                tc_fence_before();
+                mbar_arrive(&ctl.tmem_empty[buf]);
                 if (b == nb - 1) {
-                    // ---- end of sweep: annealing state machine (solvers.cpp:178-200), side 0
-                    epi_sync();                                   // walks done: Sdel is scratch
-                    if (side == 1) x_dmax[r] = dmax;
-                    epi_sync();
-                    if (side == 0) {
-                        dmax = fmaxf(dmax, x_dmax[r]);
-                        if (active) {
-                            const int code = slot_after_sweep(slot, dmax, a);
-                            if (code != kSlotContinue) {
-                                slot_finish(slot, code, a);
-                                old_run = slot.run;
-                                new_run = claim_run(a);
-                                mode = new_run >= 0 ? kLoading : kDrain;
-                            }
-                        } else if (mode == kLoading) {
-                            slot_start(slot, new_run, a);
-                            mode = kActive;
-                            old_run = -1;
-                        } else if (mode == kDrain) {
-                            mode = kIdle;
-                            old_run = -1;
+                    // ---- end of sweep: annealing state machine (solvers.cpp:178-200)
+                    if (active) {
+                        const int code = slot_after_sweep(slot, dmax, a);
+                        if (code != kSlotContinue) {
+                            slot_finish(slot, code, a);
+                            old_run = slot.run;
+                            new_run = claim_run(a);
+                            mode = new_run >= 0 ? kLoading : kDrain;
                         }
-                        quench = mode == kActive && slot_quench(slot);
-                        Tf = static_cast<float>(slot.T);
-                        rT = quench ? 0.0f : recip_for_div(Tf);
-                        x_mode[r] = mode;
-                        x_new[r] = new_run;
-                        x_old[r] = old_run;
-                        x_rT[r] = rT;
-                        x_T[r] = Tf;
-                        x_quench[r] = quench;
+                    } else if (mode == kLoading) {
+                        slot_start(slot, new_run, a);
+                        mode = kActive;
+                        old_run = -1;
+                    } else if (mode == kDrain) {
+                        mode = kIdle;
+                        old_run = -1;
                     }
-                    const bool more = epi_any(side == 0 && mode != kIdle);
-                    if (side == 1) {
-                        mode = x_mode[r];
-                        new_run = x_new[r];
-                        old_run = x_old[r];
-                        rT = x_rT[r];
-                        Tf = x_T[r];
-                        quench = x_quench[r] != 0;
-                    }
-                    if (!more && et == 0) ctl.stop = 1;
+                    quench = mode == kActive && slot_quench(slot);
+                    Tf = static_cast<float>(slot.T);
+                    rT = quench ? 0.0f : recip_for_div(Tf);
+                    const bool more = epi_any(mode != kIdle);
+                    if (!more && wt == 0) ctl.stop = 1;
                     fence_proxy_async_global();
-                    mbar_arrive(&ctl.chunk_ready);
-                    if (!more) goto epilogue_done;
+                    mbar_arrive(&ctl.chunk_ready[1]);
+                    if (!more) goto walker_done;
                 } else {
                     fence_proxy_async_global();
-                    mbar_arrive(&ctl.chunk_ready);
+                    mbar_arrive(&ctl.chunk_ready[1]);
                 }
             }
         }
-    epilogue_done:
-        if (a.prof && et == 0) {
+    walker_done:
+        if (a.prof && wt == 0) {
             long long* pr = a.prof + blockIdx.x * kProfSlots;
             pr[0] = n_sweeps;
             pr[1] = clock64() - c_start;
-            pr[2] = c_loads;
-            pr[3] = c_wait;
-            pr[4] = c_corr;
-            pr[5] = c_wb;
+            pr[2] = c_wait;
+            pr[3] = c_f;
+            pr[4] = c_apply;
+            pr[5] = c_walk;
             pr[6] = nb;
-            pr[12] = c_walk;
-            pr[13] = n_walks;
-            pr[14] = c_pass0 + (c_pass1 << 0) * 0;
-            pr[15] = c_hand;
-            pr[7] = c_pass1;
+            pr[7] = c_turn;
+            pr[12] = c_st;
+        }
+    } else {
+        // ================================================================ helpers (H)
+        // Warp w (quarter q = w % 4, same runs as walker warp w - 4) prepares the fields of
+        // sub-block t >= 2: GEMM fields + the Deltas of sub-blocks 0 .. t-2 (history in TMEM,
+        // triangle rows from smem), written back to TMEM for the walker.  It also stages the
+        // next block's diagonal triangle into the other smem buffer.
+        const int q = warp & 3;
+        const int ht = threadIdx.x - EPI_H * 32;           // 0..127
+        const std::uint32_t lane_t = static_cast<std::uint32_t>(q * 32) << 16;
+        std::uint32_t g = 0, fe = 0, de = 0;
+        long long c_dw = 0, c_work = 0, c_tw = 0;
+        issue_jtri(Jtri0, a.J32, np, 0, ht);
+        cp_async_arrive_noinc(&ctl.jready[0]);
+        for (;;) {
+            for (int b = 0; b < nb; ++b, ++g) {
+                const int b0 = b * TB;
+                const int lim = min(TB, n - b0);
+                const int nsub = (lim + SB - 1) / SB;
+                const float* jtri = Jtri0 + (g & 1) * (SMEM_TRI / 4);
+                const int buf = g & 1;
+                long long t0 = clock64();
+                mbar_wait(&ctl.jready[buf], (g >> 1) & 1);
+                mbar_wait(&ctl.tmem_full[buf], (g >> 1) & 1);
+                tc_fence_after();
+                long long t1 = clock64();
+                c_tw += t1 - t0;
+                const std::uint32_t tacc = tmem + lane_t + buf * TB;
+                bool staged = false;
+                for (int t = 2; t <= nsub + 1; ++t) {
+                    // target sub-block t (t < nsub); D-event for sub-block t-2 (t-2 = 0 always,
+                    // else only while t < nsub) -- mirrors the walker's arrivals
+                    const bool target = t < nsub;
+                    if (!target && t - 2 > 0) break;
+                    float2 pf[SB / 2];
+                    if (target) {
+                        float pv[SB];
+                        tmem_ld16(tacc + t * SB, pv);
+#pragma unroll
+                        for (int j = 0; j < SB / 2; ++j) pf[j] = make_float2(pv[2 * j], pv[2 * j + 1]);
+                        // Deltas already final: sub-blocks 0 .. t-3
+                        for (int u = 0; u + 3 <= t && !(up.exp & 1); ++u) {
+                            float du[SB];
+                            tmem_ld16(tmem + lane_t + DEL_COL + u * SB, du);
+                            apply_rect16(pf, jtri, u * SB, t * SB, du);
+                        }
+                    }
+                    t0 = clock64();
+                    c_work += t0 - t1;
+                    mbar_wait(&ctl.dready[q][de & 1], (de >> 1) & 1);
+                    ++de;
+                    tc_fence_after();
+                    t1 = clock64();
+                    c_dw += t1 - t0;
+                    if (t == 2 && !staged) {
+                        // the walker is past the previous block: stage the next block's triangle
+                        const int nb0 = (b + 1 == nb) ? 0 : b0 + TB;
+                        issue_jtri(Jtri0 + ((g + 1) & 1) * (SMEM_TRI / 4), a.J32, np, nb0, ht);
+                        cp_async_arrive_noinc(&ctl.jready[(g + 1) & 1]);
+                        staged = true;
+                    }
+                    if (!target) break;
+                    float du[SB];
+                    tmem_ld16(tmem + lane_t + DEL_COL + (t - 2) * SB, du);
+                    if (!(up.exp & 1)) apply_rect16(pf, jtri, (t - 2) * SB, t * SB, du);
+                    float pv[SB];
+#pragma unroll
+                    for (int j = 0; j < SB / 2; ++j) {
+                        pv[2 * j] = pf[j].x;
+                        pv[2 * j + 1] = pf[j].y;
+                    }
+                    tmem_st16f(tacc + t * SB, pv);
+                    tmem_st_wait();
+                    tc_fence_before();
+                    mbar_arrive(&ctl.fready[q][fe & 1]);
+                    ++fe;
+                    t0 = clock64();
+                    c_work += t0 - t1;
+                    t1 = t0;
+                }
+                if (b == nb - 1) {
+                    const bool more = epi_any(false);
+                    if (!more) goto helper_done;
+                }
+            }
+        }
+    helper_done:
+        cp_async_wait_all();
+        if (a.prof && ht == 0) {
+            long long* pr = a.prof + blockIdx.x * kProfSlots;
+            pr[13] = c_dw;
+            pr[14] = c_work;
+            pr[15] = c_tw;
         }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 1) tmem_dealloc(tmem, 2 * TB);
+    if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
 }
 
 }  // namespace
 
 int relax_dense_umma_slots_per_cta() { return TM; }
 int relax_dense_umma_block() { return TB; }
+int relax_dense_umma_kc() { return KC; }
 std::size_t relax_dense_umma_plane_rows(int grid) { return static_cast<std::size_t>(grid) * TM; }
 
 cudaError_t launch_relax_dense_umma(const RelaxArgs& a, const UmmaLaunch& u, int grid, cudaStream_t st) {
-    const char* hint = std::getenv("MARS_UMMA_L2HINT");
-    UmmaParams up{u.s_hi, u.s_hi, u.s_lo, a.np / TB, hint ? std::atoi(hint) : 1};
+    const char* ex = std::getenv("MARS_UMMA_EXP");
+    UmmaParams up{u.s_hi, u.s_hi, u.s_lo, a.np / TB, ex ? std::atoi(ex) : 0};
     if (a.np % TB != 0) return cudaErrorInvalidValue;
     cudaError_t e;
     if (u.jlo) {

@@ -204,6 +204,19 @@ __device__ __forceinline__ std::uint64_t desc_k_sw128(std::uint32_t smem_addr) {
     return d;
 }
 
+// K-major SWIZZLE_64B canonical layout (8 rows x 64 B atoms, SBO = 512 B): the layout a TMA
+// load with CU_TENSOR_MAP_SWIZZLE_64B and a 32-element fp16 box row produces.  Tile base
+// 512-byte aligned; advancing K by 16 fp16 adds 32 B to the start address.
+__device__ __forceinline__ std::uint64_t desc_k_sw64(std::uint32_t smem_addr) {
+    std::uint64_t d = 0;
+    d |= static_cast<std::uint64_t>((smem_addr >> 4) & 0x3FFFu);
+    d |= static_cast<std::uint64_t>(1u) << 16;                 // LBO (ignored for swizzled K-major)
+    d |= static_cast<std::uint64_t>(512u >> 4) << 32;          // SBO
+    d |= static_cast<std::uint64_t>(1u) << 46;                 // version = 1 (sm_100)
+    d |= static_cast<std::uint64_t>(4u) << 61;                 // SWIZZLE_64B
+    return d;
+}
+
 // Instruction descriptor, kind::f16: A/B fp16 (fmt 0) or bf16 (fmt 1), D fp32, both K-major.
 __host__ __device__ constexpr std::uint32_t idesc_f16(int M, int N, int ab_format = 0) {
     return (1u << 4)                                   // D format f32
@@ -249,6 +262,76 @@ __device__ __forceinline__ void tmem_st16(std::uint32_t taddr, const std::uint32
 
 __device__ __forceinline__ void tmem_st_wait() {
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+
+}  // namespace umma
+}  // namespace marsb200
+
+namespace marsb200 {
+namespace umma {
+
+// ---- warp-converged issue: the whole warp executes these, one elected lane issues.  The
+// operands are warp-uniform, so they stay in uniform registers and no per-instruction
+// "waterfall" loop is generated (a single-lane `if (lane == 0)` issue loop costs ~100+
+// instructions per pipeline stage and was measured to bound the GEMM at ~40% of the pipe).
+
+__device__ __forceinline__ void mma_f16_ss_elect(std::uint32_t d_tmem, std::uint64_t adesc, std::uint64_t bdesc,
+                                                 std::uint32_t idesc, std::uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t"
+        "setp.ne.b32 q, %4, 0;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\n\t}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_commit_elect(std::uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx_elect(std::uint64_t* bar, std::uint32_t bytes) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b64 st;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(smem_u32(bar)),
+        "r"(bytes)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_elect(std::uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b64 st;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p mbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_elect(std::uint32_t smem_dst, const void* tmap, std::uint32_t bar,
+                                                  int c0, int c1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4}], [%2];\n\t}\n" ::"r"(smem_dst),
+        "l"(reinterpret_cast<std::uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_hint_elect(std::uint32_t smem_dst, const void* tmap, std::uint32_t bar,
+                                                       int c0, int c1, std::uint64_t policy) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%3, %4}], [%2], %5;\n\t}\n" ::"r"(smem_dst),
+        "l"(reinterpret_cast<std::uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
 }
 
 }  // namespace umma
