@@ -824,3 +824,24 @@ int orc_replay_batch_f32(const void* vp, const orc_params_t* prm, int64_t runs, 
     free(hf);
     return 0;
 }
+
+/* TEST-ONLY: mars_relax_sweep (solvers.cpp:150-161) in fp32 -- fp32 state, row dot accumulated
+ * in fp32 in ascending j, tanhf -- the single-sweep fp32 floor the device trajectory gates of
+ * tests/test_gpu_trajectory.py are set from (dense problems only; returns d). */
+double orc_relax_sweep_f32(const void* vp, float* s, double t) {
+    const orc_problem* p = (const orc_problem*)vp;
+    const int n = p->n;
+    const float tf = (float)t;
+    float d = 0.0f;
+    for (int i = 0; i < n; ++i) {
+        const double* row = p->J + (size_t)i * n;
+        float phi = 0.0f;
+        for (int j = 0; j < n; ++j) phi = fmaf((float)row[j], s[j], phi);
+        phi += (float)p->h[i];
+        const float trial = t < K_TEMP_FLOOR ? (phi > 0.0f ? -1.0f : (phi < 0.0f ? 1.0f : 0.0f)) : -tanhf(phi / tf);
+        const float dd = fabsf(trial - s[i]);
+        d = d > dd ? d : dd;
+        s[i] = trial;
+    }
+    return d;
+}

@@ -97,6 +97,7 @@ ORC_DECLARE(orc_)
 void orc_set_sweep_cap(int64_t cap);
 /* TEST-ONLY measurement tool (mars_oracle.c): the reference descent replayed in fp32
  * (mode 0) or fp32 with J rounded to one fp16 plane (mode 1); dense problems only. */
+double orc_relax_sweep_f32(const void* p, float* s, double t);
 int orc_replay_batch_f32(const void* p, const orc_params_t* prm, int64_t runs, uint64_t base_seed,
                          int workers, int mode, uint8_t* status, int64_t* iters, int8_t* spins);
 

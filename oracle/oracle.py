@@ -113,6 +113,9 @@ class Oracle:
         self._gen_er = f("gen_er", i64, i32, dbl, u64, vp, vp, vp)
         self._gen_ea = f("gen_ea", i64, i32, i32, u64, vp, vp, vp)
         if kind == "port":
+            self._sweep32 = L.orc_relax_sweep_f32
+            self._sweep32.restype = dbl
+            self._sweep32.argtypes = [vp, vp, dbl]
             self._replay = L.orc_replay_batch_f32
             self._replay.restype = i32
             self._replay.argtypes = [vp, C.POINTER(OracleParams), i64, u64, i32, i32, vp, vp, vp]
@@ -267,6 +270,11 @@ class OracleProblem:
             raise OracleError(1, err.value.decode())
         return dict(status=int(st[0]), energy=float(e[0]), cut=float(c[0]),
                     descent_iters=int(it[0]), spins=sp)
+
+    def relax_sweep_f32(self, s: np.ndarray, t: float) -> float:
+        """Port only (TEST-ONLY): one in-order sweep in fp32 (the fp32 floor), in place."""
+        assert s.dtype == np.float32 and s.flags.c_contiguous
+        return self.orc._sweep32(self.h, _ptr(s), t)
 
     def replay_f32(self, prm: OracleParams, runs: int, base_seed: int, workers: int = 0, mode: int = 0):
         """Port only (TEST-ONLY measurement tool): the first `runs` descents replayed with fp32

@@ -81,8 +81,8 @@ int relax_dense_simt_slots_per_cta();
 int relax_dense_simt_block();
 std::size_t relax_dense_simt_work_bytes(int np);
 
-// tcgen05 dense kernel: TMA maps over the fp16 state planes ([grid*128][np], per batch)
-// and the fp16 coupling planes ([np][np], per problem).
+// tcgen05 dense kernel (CTA pairs: grid must be even): TMA maps over the fp16 state planes
+// ([grid*128][np], per batch) and the fp16 coupling planes ([np][np], per problem).
 struct UmmaLaunch {
     CUtensorMap tm_shi, tm_slo, tm_jhi, tm_jlo;
     __half* s_hi;
@@ -93,6 +93,7 @@ cudaError_t launch_relax_dense_umma(const RelaxArgs& a, const UmmaLaunch& u, int
 int relax_dense_umma_slots_per_cta();
 int relax_dense_umma_block();
 int relax_dense_umma_kc();      // K per pipeline stage (the TMA box width of both operand maps)
+int relax_dense_umma_j_rows();  // coupling-tile rows per CTA of the pair (TMA box height of J maps)
 std::size_t relax_dense_umma_plane_rows(int grid);
 
 // Level-scheduled sparse kernel (relax_csr.cu).  Spins grouped by Gauss-Seidel level,

@@ -478,8 +478,8 @@ int build_device_store(mars_problem* p) {
             if (int rc = upload(&p->dJhi, jh.data(), jh.size())) return rc;
             if (int rc = upload(&p->dJlo, jl.data(), jl.size())) return rc;
             const int tb = relax_dense_umma_block();
-            if (!make_tmap_f16(&p->tm_jhi, p->dJhi, p->np, p->np, relax_dense_umma_kc(), tb) ||
-                !make_tmap_f16(&p->tm_jlo, p->dJlo, p->np, p->np, relax_dense_umma_kc(), tb))
+            if (!make_tmap_f16(&p->tm_jhi, p->dJhi, p->np, p->np, relax_dense_umma_kc(), relax_dense_umma_j_rows()) ||
+                !make_tmap_f16(&p->tm_jlo, p->dJlo, p->np, p->np, relax_dense_umma_kc(), relax_dense_umma_j_rows()))
                 return fail(MARS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the coupling planes");
         }
     } else {
@@ -778,17 +778,17 @@ int batch_alloc(mars_batch* b) {
         } else {
             tm = relax_dense_umma_slots_per_cta();
             per_cta = static_cast<std::size_t>(2) * tm * p->np * sizeof(__half);   // S_hi + S_lo rows
-            // Persistent CTAs: when the fp16 J planes fit in L2, only as many CTAs as keep
-            // their state planes (re-read by every spin block's GEMM) in L2 beside J.  The
-            // kernel runs power-capped, so fewer CTAs also clock higher: cfg2 (N = 2000)
-            // measured 11.6K descents/s at 148 CTAs, 12.2K at 96-104 (this rule: 104), 11.1K
-            // at 64.  MARS_UMMA_GRID overrides.
+            // Persistent CTAs (in pairs): when the fp16 J planes fit in L2, only as many CTAs as
+            // keep their state planes (re-read by every spin block's GEMM) in 85% of L2 beside
+            // J.  cfg2 (N = 2000, round 2 kernel) measured 11.5K descents/s at 148 CTAs, 12.6K
+            // at 110, 12.8K at 96 (this rule: 96).  MARS_UMMA_GRID overrides.
             int l2 = 0;
             cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, p->device);
             const std::size_t jbytes = static_cast<std::size_t>(2) * p->np * p->np * sizeof(__half);
             int fit = p->num_sms;
-            if (l2 > 0 && jbytes < static_cast<std::size_t>(l2))
-                fit = static_cast<int>((static_cast<std::size_t>(l2) - jbytes) / per_cta);
+            const std::size_t l2use = static_cast<std::size_t>(l2) * 85 / 100;   // headroom: J32 diag, s0, spins
+            if (l2 > 0 && jbytes < l2use)
+                fit = static_cast<int>((l2use - jbytes) / per_cta);
             fit = std::max(p->num_sms / 2, std::min(p->num_sms, fit));
             max_grid = std::max(1, std::min(p->num_sms, env_int("MARS_UMMA_GRID", fit)));
         }
@@ -826,6 +826,8 @@ int batch_alloc(mars_batch* b) {
         }
     }
     b->grid = std::max(1, std::min(max_grid, (b->queue_len + tm - 1) / tm));
+    if (p->kernel == MARS_KERNEL_DENSE_UMMA && !b->use_small)
+        b->grid = std::max(2, b->grid + (b->grid & 1));   // CTA pairs (cta_group::2)
     b->sparse.grid = b->grid;
     b->spmm.grid = b->grid;
     b->stencil.grid = b->grid;

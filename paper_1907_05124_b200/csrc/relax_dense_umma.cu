@@ -68,13 +68,17 @@ constexpr int TB = 128;      // spins per Gauss-Seidel block = UMMA N
 // former 2 x 64 KB ring kept ~1 (measured: the MMA waited on TMA, not on SMEM or the pipe).
 constexpr int KC = 32;
 constexpr int CPB = TB / KC; // chunks per block
-constexpr int STAGES = 5;
+constexpr int STAGES = 6;
 constexpr int NT = 320;      // 2 control warps + 4 walker warps + 4 helper warps
 constexpr int EPI_W = 2;     // first walker warp
 constexpr int EPI_H = 6;     // first helper warp
 constexpr int NW = 128;      // walker (= helper) threads
+// CTA pair (cluster of 2, cta_group::2): the leader issues M = 2*TM MMAs; each CTA holds its own
+// TM state rows and half (TB/2 rows) of every coupling tile, so each SM loads and feeds to the
+// tensor core only half of J -- the operand stream per SM per block drops by a quarter.
+constexpr int TBH = TB / 2;  // coupling rows per CTA of the pair
 constexpr std::uint32_t TILE_A = TM * KC * 2;   // 8 KB
-constexpr std::uint32_t TILE_J = TB * KC * 2;   // 8 KB
+constexpr std::uint32_t TILE_J = TBH * KC * 2;  // 4 KB
 constexpr std::uint32_t STAGE_BYTES = 2 * TILE_A + 2 * TILE_J;
 // TMEM: two 128-column field accumulators (ping-pong across blocks) + the current block's
 // Delta history (one column per spin, lane = run)
@@ -93,6 +97,9 @@ struct __align__(8) Ctl {
     std::uint64_t fready[4][2];     // helper -> walker: pre-corrected fields (per lane quarter)
     std::uint64_t dready[4][2];     // walker -> helper: a sub-block's Deltas in TMEM
     std::uint64_t mma_done;
+    std::uint64_t pair_more[2];     // end-of-sweep consensus with the peer CTA (per sweep parity)
+    std::uint32_t peer_more[2];     // written remotely by the peer
+    std::uint32_t more_all;
     std::uint32_t tmem_base;
     volatile std::uint32_t stop;
     volatile std::uint32_t poison;  // producer stopped: the stage it arrived on carries no data
@@ -131,7 +138,8 @@ struct UmmaParams {
     __half* s_hi_w;
     __half* s_lo_w;
     int nb;                  // blocks per sweep = np / TB
-    int exp;                 // EXPERIMENT knobs (MARS_UMMA_EXP): 1 = no epilogue arithmetic, 2 = no J_lo product
+    int pf;                  // L2 prefetch distance of the state tiles, in chunks (0 = off; measured
+                             // slower on cfg2 at 8 and 16 -- extra L2 pressure), MARS_UMMA_PF
 };
 
 __device__ __forceinline__ void split16(float v, __half& hi, __half& lo, float& back) {
@@ -195,8 +203,8 @@ __device__ __forceinline__ void sub_update(float2 (&p)[SB / 2], const float4 (&j
 }
 
 template <int I, bool FULL, bool HAS_H>
-__device__ __forceinline__ void sub_step(float2 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB],
-                                         float (&del)[SB], int k0, SubCtx& c) {
+__device__ __forceinline__ void sub_step(float2 (&p)[SB / 2], float2 (&an)[SB / 2], const float (&old)[SB],
+                                         float (&nv)[SB], float (&del)[SB], int k0, SubCtx& c) {
     if (FULL || k0 + I < c.lim) {
         // J[k0+I][k0 + 4g ..] for the groups this spin updates, issued before the trial
         float4 jr[SB / 4];
@@ -219,6 +227,15 @@ __device__ __forceinline__ void sub_step(float2 (&p)[SB / 2], const float (&old)
         c.dmax = fmaxf(c.dmax, fabsf(delta));
         if constexpr (I + 1 < SB)
             sub_update<I>(p, jr, delta, std::make_integer_sequence<int, SB / 4 - ((I + 1) & ~3) / 4>{});
+        // this spin's coupling to the NEXT sub-block's fields, accumulated off the serial chain
+        // (fills the walk's idle issue slots; added to the next sub-block's fields before it walks)
+        const float4* jn = reinterpret_cast<const float4*>(tri_ptr(c.jtri, k0 + I, k0 + SB));
+#pragma unroll
+        for (int g = 0; g < SB / 4; ++g) {
+            const float4 jv = jn[g];
+            an[2 * g] = ffma2(make_float2(jv.x, jv.y), delta, an[2 * g]);
+            an[2 * g + 1] = ffma2(make_float2(jv.z, jv.w), delta, an[2 * g + 1]);
+        }
     } else {
         nv[I] = old[I];
         del[I] = 0.0f;
@@ -226,18 +243,19 @@ __device__ __forceinline__ void sub_step(float2 (&p)[SB / 2], const float (&old)
 }
 
 template <bool FULL, bool HAS_H, int... I>
-__device__ __forceinline__ void sub_walk(float2 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB],
-                                         float (&del)[SB], int k0, SubCtx& c, std::integer_sequence<int, I...>) {
-    (sub_step<I, FULL, HAS_H>(p, old, nv, del, k0, c), ...);
+__device__ __forceinline__ void sub_walk(float2 (&p)[SB / 2], float2 (&an)[SB / 2], const float (&old)[SB],
+                                         float (&nv)[SB], float (&del)[SB], int k0, SubCtx& c,
+                                         std::integer_sequence<int, I...>) {
+    (sub_step<I, FULL, HAS_H>(p, an, old, nv, del, k0, c), ...);
 }
 
 template <bool HAS_H>
-__device__ __forceinline__ void walk_dispatch(float2 (&p)[SB / 2], const float (&old)[SB], float (&nv)[SB],
-                                              float (&del)[SB], int k0, SubCtx& c) {
+__device__ __forceinline__ void walk_dispatch(float2 (&p)[SB / 2], float2 (&an)[SB / 2], const float (&old)[SB],
+                                              float (&nv)[SB], float (&del)[SB], int k0, SubCtx& c) {
     if (k0 + SB <= c.lim)
-        sub_walk<true, HAS_H>(p, old, nv, del, k0, c, std::make_integer_sequence<int, SB>{});
+        sub_walk<true, HAS_H>(p, an, old, nv, del, k0, c, std::make_integer_sequence<int, SB>{});
     else
-        sub_walk<false, HAS_H>(p, old, nv, del, k0, c, std::make_integer_sequence<int, SB>{});
+        sub_walk<false, HAS_H>(p, an, old, nv, del, k0, c, std::make_integer_sequence<int, SB>{});
 }
 
 // fields (fp32 pairs) += J[j0 .. j0+16)[col .. col+16)^T * d[0..16): the 16 x 16 rectangle
@@ -335,6 +353,23 @@ __device__ __forceinline__ void issue_jtri(float* dst, const float* J32, int np,
     }
 }
 
+// End-of-sweep consensus of the CTA pair (walkers + helpers of both CTAs): the pair runs its
+// blocks in lock step (one MMA stream), so it stops only when neither CTA has a slot left.
+// Called by all 256 epilogue threads with their CTA-local vote; `lead` is one walker thread.
+__device__ __forceinline__ bool pair_any(Ctl& ctl, bool local, bool lead, std::uint32_t rank, long long sweep) {
+    // sweep: 0-based index; consecutive sweeps alternate between two barrier/flag slots
+    const std::uint32_t par = static_cast<std::uint32_t>(sweep) & 1u;
+    if (lead) {
+        const std::uint32_t peer = rank ^ 1u;
+        st_cluster_u32(mapa_shared(smem_u32(&ctl.peer_more[par]), peer), local ? 1u : 0u);
+        mbar_arrive_cluster(mapa_shared(smem_u32(&ctl.pair_more[par]), peer));
+        mbar_wait_cluster(&ctl.pair_more[par], (static_cast<std::uint32_t>(sweep) >> 1) & 1u);
+        ctl.more_all = (local || ctl.peer_more[par] != 0) ? 1u : 0u;
+    }
+    asm volatile("bar.sync 1, 256;\n" ::: "memory");
+    return ctl.more_all != 0;
+}
+
 template <bool JLO>
 __global__ void __launch_bounds__(NT, 1)
 relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUtensorMap tm_shi,
@@ -358,7 +393,8 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&ctl.tmem_full[s], 1);
-            mbar_init(&ctl.tmem_empty[s], NW);
+            mbar_init(&ctl.tmem_empty[s], 2 * NW);   // leader's: both CTAs' walkers
+            mbar_init(&ctl.pair_more[s], 1);
             mbar_init(&ctl.chunk_ready[s], NW);
             mbar_init(&ctl.jready[s], NW);
         }
@@ -372,7 +408,10 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         ctl.poison = 0;
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc(&ctl.tmem_base, TMEM_COLS);
+    const std::uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    cluster_sync_all();                      // the peer's barriers exist before any remote arrive
+    if (warp == 1) tmem_alloc_pair(&ctl.tmem_base, TMEM_COLS);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -390,9 +429,10 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         }
         __syncwarp();
         const std::uint64_t jpol = policy_evict_last();
+        const std::uint64_t spol = policy_evict_normal();
         const std::uint32_t smem0 = smem_u32(base);
         const std::uint32_t full0 = smem_u32(&ctl.full[0]);
-        const std::uint32_t tx = JLO ? STAGE_BYTES : STAGE_BYTES - TILE_J;
+        const std::uint32_t tx = 2 * (JLO ? STAGE_BYTES : STAGE_BYTES - TILE_J);   // both CTAs' bytes
         std::uint32_t g = 0, s = 0, ph = 0;
         long long w_ready = 0, w_empty = 0;
         for (;;) {
@@ -409,8 +449,10 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         if (half == 1 && ctl.stop) {
                             mbar_wait(&ctl.empty[s], ph ^ 1);
                             if (lane == 0) {
-                                ctl.poison = 1;
-                                mbar_arrive(&ctl.full[s]);
+                                if (leader) {
+                                    ctl.poison = 1;
+                                    mbar_arrive(&ctl.full[s]);
+                                }
                                 if (a.prof) {
                                     a.prof[blockIdx.x * kProfSlots + 8] = w_ready;
                                     a.prof[blockIdx.x * kProfSlots + 9] = w_empty;
@@ -424,13 +466,24 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     w_empty += clock64() - t1;
                     const std::uint32_t st = smem0 + s * STAGE_BYTES;
                     const std::uint32_t fb = full0 + s * 8;
-                    mbar_arrive_expect_tx_elect(&ctl.full[s], tx);
-                    tma_load_2d_elect(st, &tm_shi, fb, c * KC, row0);
-                    tma_load_2d_elect(st + TILE_A, &tm_slo, fb, c * KC, row0);
+                    if (leader) mbar_arrive_expect_tx_elect(&ctl.full[s], tx);
+                    tma_load_2d_pair_elect(st, &tm_shi, fb, c * KC, row0, spol);
+                    tma_load_2d_pair_elect(st + TILE_A, &tm_slo, fb, c * KC, row0, spol);
                     // the coupling tiles are read by every CTA every sweep: keep them in L2
-                    // ahead of the per-CTA state planes
-                    tma_load_2d_hint_elect(st + 2 * TILE_A, &tm_jhi, fb, c * KC, b * TB, jpol);
-                    if (JLO) tma_load_2d_hint_elect(st + 2 * TILE_A + TILE_J, &tm_jlo, fb, c * KC, b * TB, jpol);
+                    // ahead of the per-CTA state planes; this CTA's half of the block's rows
+                    tma_load_2d_pair_elect(st + 2 * TILE_A, &tm_jhi, fb, c * KC, b * TB + rank * TBH, jpol);
+                    if (JLO) tma_load_2d_pair_elect(st + 2 * TILE_A + TILE_J, &tm_jlo, fb, c * KC, b * TB + rank * TBH, jpol);
+                    if (up.pf > 0) {
+                        // warm L2 with this CTA's state tiles up.pf chunks ahead (same block;
+                        // a chunk of block b-1 fetched early is refreshed in L2 by the walker's
+                        // write-back, so the later TMA load still reads the new values)
+                        int cp = c + up.pf;
+                        if (cp >= nk) cp -= nk;
+                        if (j + up.pf < nk) {
+                            tma_prefetch_2d_elect(&tm_shi, cp * KC, row0);
+                            tma_prefetch_2d_elect(&tm_slo, cp * KC, row0);
+                        }
+                    }
                     if (++c == nk) c = 0;
                     if (++s == STAGES) {
                         s = 0;
@@ -442,9 +495,11 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
     producer_done:;
     } else if (warp == 1) {
         // ================================================================ MMA issuer
-        // Whole warp converged (descriptors are warp-uniform: uniform registers); one
-        // elected lane issues each tcgen05.mma / commit.
-        constexpr std::uint32_t idesc = idesc_f16(TM, TB, 0);
+        // Leader CTA only.  Whole warp converged (descriptors are warp-uniform: uniform
+        // registers); one elected lane issues each tcgen05.mma / commit for the pair.
+        if (!leader) goto mma_skip;
+        {
+        constexpr std::uint32_t idesc = idesc_f16(2 * TM, TB, 0);
         const std::uint32_t smem0 = smem_u32(base);
         std::uint32_t g = 0, s = 0, ph = 0;
         long long w_full = 0, w_tmem = 0;
@@ -475,25 +530,27 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         const std::uint64_t ahi = desc_k_sw64(st + kk * 32);
                         const std::uint64_t alo = desc_k_sw64(st + TILE_A + kk * 32);
                         const std::uint64_t jhi = desc_k_sw64(st + 2 * TILE_A + kk * 32);
-                        mma_f16_ss_elect(d, ahi, jhi, idesc, (j | kk) != 0);
-                        mma_f16_ss_elect(d, alo, jhi, idesc, 1);
-                        if (JLO && !(up.exp & 2)) {
+                        mma_f16_ss_pair_elect(d, ahi, jhi, idesc, (j | kk) != 0);
+                        mma_f16_ss_pair_elect(d, alo, jhi, idesc, 1);
+                        if (JLO) {
                             const std::uint64_t jlo = desc_k_sw64(st + 2 * TILE_A + TILE_J + kk * 32);
-                            mma_f16_ss_elect(d, ahi, jlo, idesc, 1);
+                            mma_f16_ss_pair_elect(d, ahi, jlo, idesc, 1);
                         }
                     }
-                    mma_commit_elect(&ctl.empty[s]);
+                    mma_commit_pair_mc_elect(&ctl.empty[s]);
                     if (++s == STAGES) {
                         s = 0;
                         ph ^= 1;
                     }
                 }
-                mma_commit_elect(&ctl.tmem_full[buf]);
+                mma_commit_pair_mc_elect(&ctl.tmem_full[buf]);
             }
         }
     mma_done:
-        mma_commit_elect(&ctl.mma_done);
+        mma_commit_pair_mc_elect(&ctl.mma_done);
         mbar_wait(&ctl.mma_done, 0);
+        }
+    mma_skip:
         __syncwarp();
     } else if (warp < EPI_H) {
         // ================================================================ walkers (W)
@@ -515,6 +572,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         float rT = 1.0f, Tf = 1.0f;
         bool quench = false;
         std::uint32_t g = 0, fe = 0, de = 0;                // block, F-event and D-event counters
+        const std::uint32_t tmem_empty_leader = mapa_shared(smem_u32(&ctl.tmem_empty[0]), 0);
         long long c_wait = 0, c_f = 0, c_apply = 0, c_walk = 0, c_turn = 0, c_st = 0, n_sweeps = 0;
         const long long c_start = clock64();
 
@@ -567,7 +625,10 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 c_wait += t0 - t1;
                 const std::uint32_t tacc = tmem + lane_t + buf * TB;
                 SubCtx ctx{jtri, a.h32 ? a.h32 + b0 : nullptr, Tf, rT, quench, lim, 0.0f};
-                float prev[SB];                                 // Deltas of sub-block t-1
+                float prev[SB];                                 // this sub-block's Deltas
+                float2 an[SB / 2];                              // previous sub-block's coupling
+#pragma unroll                                                  // to this one (built during its walk)
+                for (int j = 0; j < SB / 2; ++j) an[j] = make_float2(0.0f, 0.0f);
                 for (int t = 0; t < nsub; ++t) {
                     const int k0 = t * SB;
                     float old[SB];
@@ -583,19 +644,16 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     tmem_ld16(tacc + k0, pv);
                     float2 pf[SB / 2];
 #pragma unroll
-                    for (int j = 0; j < SB / 2; ++j) pf[j] = make_float2(pv[2 * j], pv[2 * j + 1]);
+                    for (int j = 0; j < SB / 2; ++j) {
+                        pf[j] = make_float2(pv[2 * j] + an[j].x, pv[2 * j + 1] + an[j].y);
+                        an[j] = make_float2(0.0f, 0.0f);
+                    }
                     t0 = clock64();
                     c_f += t0 - t1;
-                    if (t >= 1 && !(up.exp & 1)) apply_rect16(pf, jtri, k0 - SB, k0, prev);
-                    t1 = clock64();
-                    c_apply += t1 - t0;
+                    t1 = t0;
                     float nv[SB];
-                    if (up.exp & 1) {
-#pragma unroll
-                        for (int j = 0; j < SB; ++j) { nv[j] = old[j]; prev[j] = 0.0f; }
-                        ctx.dmax = fmaxf(ctx.dmax, pf[0].x * 1e-30f);
-                    } else if (ctx.h) walk_dispatch<true>(pf, old, nv, prev, k0, ctx);
-                    else walk_dispatch<false>(pf, old, nv, prev, k0, ctx);
+                    if (ctx.h) walk_dispatch<true>(pf, an, old, nv, prev, k0, ctx);
+                    else walk_dispatch<false>(pf, an, old, nv, prev, k0, ctx);
                     t0 = clock64();
                     c_walk += t0 - t1;
                     if (active) store_new16(hi_row + b0 + k0, lo_row + b0 + k0, nv);
@@ -616,7 +674,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 }
                 dmax = fmaxf(dmax, ctx.dmax);
                 tc_fence_before();
-                mbar_arrive(&ctl.tmem_empty[buf]);
+                mbar_arrive_cluster(tmem_empty_leader + buf * 8);   // the leader's MMA reuses the buffer
                 if (b == nb - 1) {
                     // ---- end of sweep: annealing state machine (solvers.cpp:178-200)
                     if (active) {
@@ -638,7 +696,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     quench = mode == kActive && slot_quench(slot);
                     Tf = static_cast<float>(slot.T);
                     rT = quench ? 0.0f : recip_for_div(Tf);
-                    const bool more = epi_any(mode != kIdle);
+                    const bool more = pair_any(ctl, epi_any(mode != kIdle), wt == 0, rank, n_sweeps - 1);
                     if (!more && wt == 0) ctl.stop = 1;
                     fence_proxy_async_global();
                     mbar_arrive(&ctl.chunk_ready[1]);
@@ -672,7 +730,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         const int ht = threadIdx.x - EPI_H * 32;           // 0..127
         const std::uint32_t lane_t = static_cast<std::uint32_t>(q * 32) << 16;
         std::uint32_t g = 0, fe = 0, de = 0;
-        long long c_dw = 0, c_work = 0, c_tw = 0;
+        long long c_dw = 0, c_work = 0, c_tw = 0, h_sweeps = 0;
         issue_jtri(Jtri0, a.J32, np, 0, ht);
         cp_async_arrive_noinc(&ctl.jready[0]);
         for (;;) {
@@ -702,7 +760,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
 #pragma unroll
                         for (int j = 0; j < SB / 2; ++j) pf[j] = make_float2(pv[2 * j], pv[2 * j + 1]);
                         // Deltas already final: sub-blocks 0 .. t-3
-                        for (int u = 0; u + 3 <= t && !(up.exp & 1); ++u) {
+                        for (int u = 0; u + 3 <= t; ++u) {
                             float du[SB];
                             tmem_ld16(tmem + lane_t + DEL_COL + u * SB, du);
                             apply_rect16(pf, jtri, u * SB, t * SB, du);
@@ -725,7 +783,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     if (!target) break;
                     float du[SB];
                     tmem_ld16(tmem + lane_t + DEL_COL + (t - 2) * SB, du);
-                    if (!(up.exp & 1)) apply_rect16(pf, jtri, (t - 2) * SB, t * SB, du);
+                    apply_rect16(pf, jtri, (t - 2) * SB, t * SB, du);
                     float pv[SB];
 #pragma unroll
                     for (int j = 0; j < SB / 2; ++j) {
@@ -742,7 +800,8 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     t1 = t0;
                 }
                 if (b == nb - 1) {
-                    const bool more = epi_any(false);
+                    ++h_sweeps;
+                    const bool more = pair_any(ctl, epi_any(false), false, rank, h_sweeps - 1);
                     if (!more) goto helper_done;
                 }
             }
@@ -758,8 +817,9 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
     }
     tc_fence_before();
     __syncthreads();
+    cluster_sync_all();                      // both CTAs done with the pair's TMEM
     tc_fence_after();
-    if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+    if (warp == 1) tmem_dealloc_pair(tmem, TMEM_COLS);
 }
 
 }  // namespace
@@ -767,23 +827,30 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
 int relax_dense_umma_slots_per_cta() { return TM; }
 int relax_dense_umma_block() { return TB; }
 int relax_dense_umma_kc() { return KC; }
+int relax_dense_umma_j_rows() { return TBH; }
 std::size_t relax_dense_umma_plane_rows(int grid) { return static_cast<std::size_t>(grid) * TM; }
 
 cudaError_t launch_relax_dense_umma(const RelaxArgs& a, const UmmaLaunch& u, int grid, cudaStream_t st) {
-    const char* ex = std::getenv("MARS_UMMA_EXP");
-    UmmaParams up{u.s_hi, u.s_hi, u.s_lo, a.np / TB, ex ? std::atoi(ex) : 0};
-    if (a.np % TB != 0) return cudaErrorInvalidValue;
-    cudaError_t e;
-    if (u.jlo) {
-        e = cudaFuncSetAttribute(relax_dense_umma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
-        if (e != cudaSuccess) return e;
-        relax_dense_umma_kernel<true><<<grid, NT, SMEM_TOTAL, st>>>(a, up, u.tm_shi, u.tm_slo, u.tm_jhi, u.tm_jlo);
-    } else {
-        e = cudaFuncSetAttribute(relax_dense_umma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
-        if (e != cudaSuccess) return e;
-        relax_dense_umma_kernel<false><<<grid, NT, SMEM_TOTAL, st>>>(a, up, u.tm_shi, u.tm_slo, u.tm_jhi, u.tm_jlo);
-    }
-    return cudaGetLastError();
+    const char* pf = std::getenv("MARS_UMMA_PF");
+    UmmaParams up{u.s_hi, u.s_hi, u.s_lo, a.np / TB, pf ? std::atoi(pf) : 0};
+    if (a.np % TB != 0 || grid % 2 != 0) return cudaErrorInvalidValue;
+    void (*kern)(RelaxArgs, UmmaParams, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap) =
+        u.jlo ? relax_dense_umma_kernel<true> : relax_dense_umma_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = SMEM_TOTAL;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;        // the cta_group::2 pair
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a, up, u.tm_shi, u.tm_slo, u.tm_jhi, u.tm_jlo);
 }
 
 }  // namespace marsb200

@@ -93,6 +93,11 @@ __device__ __forceinline__ std::uint64_t policy_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
     return pol;
 }
+__device__ __forceinline__ std::uint64_t policy_evict_normal() {
+    std::uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ std::uint64_t policy_evict_first() {
     std::uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
@@ -331,6 +336,113 @@ __device__ __forceinline__ void tma_load_2d_hint_elect(std::uint32_t smem_dst, c
         "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
         "[%0], [%1, {%3, %4}], [%2], %5;\n\t}\n" ::"r"(smem_dst),
         "l"(reinterpret_cast<std::uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+
+}  // namespace umma
+}  // namespace marsb200
+
+namespace marsb200 {
+namespace umma {
+
+// ---- CTA pair (cluster of 2, cta_group::2): the leader (rank 0) issues M = 256 MMAs whose A
+// rows come half from each CTA's shared memory and whose B (N) columns are split between the
+// two CTAs' shared memory; each CTA's TMEM holds its own 128 rows of the accumulator.
+
+__device__ __forceinline__ std::uint32_t cluster_ctarank() {
+    std::uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// shared::cta address -> the same object's shared::cluster address in CTA `rank`
+__device__ __forceinline__ std::uint32_t mapa_shared(std::uint32_t addr, std::uint32_t rank) {
+    std::uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(std::uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+
+__device__ __forceinline__ void st_cluster_u32(std::uint32_t cluster_addr, std::uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+
+// wait with cluster-scope acquire (data written by the peer CTA before its remote arrive)
+__device__ __forceinline__ void mbar_wait_cluster(std::uint64_t* bar, std::uint32_t parity) {
+    std::uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+
+__device__ __forceinline__ void tmem_alloc_pair(std::uint32_t* dst_smem, std::uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_dealloc_pair(std::uint32_t taddr, std::uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+__device__ __forceinline__ void mma_f16_ss_pair_elect(std::uint32_t d_tmem, std::uint64_t adesc, std::uint64_t bdesc,
+                                                      std::uint32_t idesc, std::uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t"
+        "setp.ne.b32 q, %4, 0;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, q;\n\t}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// commit the pair's MMAs to the barrier at the same offset in both CTAs
+__device__ __forceinline__ void mma_commit_pair_mc_elect(std::uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b16 m;\n\t"
+        "mov.b16 m, 3;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}\n" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+// L2 prefetch of a 2D tensor tile (no shared memory, no completion): raises memory-level
+// parallelism ahead of the ring (elected lane)
+__device__ __forceinline__ void tma_prefetch_2d_elect(const void* tmap, int c0, int c1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n\t}\n" ::"l"(
+            reinterpret_cast<std::uint64_t>(tmap)),
+        "r"(c0), "r"(c1)
+        : "memory");
+}
+
+// 2-SM TMA load: into this CTA's shared memory, transaction bytes counted on the LEADER's
+// barrier (the peer bit of the barrier address cleared)
+__device__ __forceinline__ void tma_load_2d_pair_elect(std::uint32_t smem_dst, const void* tmap, std::uint32_t bar,
+                                                       int c0, int c1, std::uint64_t policy) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%3, %4}], [%2], %5;\n\t}\n" ::"r"(smem_dst),
+        "l"(reinterpret_cast<std::uint64_t>(tmap)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1), "l"(policy)
         : "memory");
 }
 

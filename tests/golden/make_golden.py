@@ -190,6 +190,16 @@ def sweeps():
                 res[ti, k] = s
         out[name + "_out"] = res
         out[name + "_d"] = ds
+        # the fp32 floor: the same sweep in fp32 (C port, ascending-j fp32 row dots, tanhf)
+        P = Oracle("port")
+        pp = P.problem_dense(gen())
+        f32 = np.zeros((len(temps), nseeds))
+        for ti, T in enumerate(temps):
+            for k, sd in enumerate(seeds):
+                s = R.initial_state(int(sd), n).astype(np.float32)
+                pp.relax_sweep_f32(s, T)
+                f32[ti, k] = np.abs(s.astype(np.float64) - res[ti, k]).max()
+        out[name + "_f32err"] = f32
         print(f"sweeps {name}: {time.time() - t:.1f}s")
     save("sweeps", **out)
 

@@ -23,10 +23,23 @@ pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
 
 SPIN_FRACTION = 0.98          # fp64 CSR kernel (exact op order) and small dense instances
-# Dense fp32 kernel on Gaussian SK N=2000, T up to 40: an fp32 replay of the reference on the
-# CPU (same order, fp32 state/fields) keeps 81% (26/32) of final spin vectors; the blocked
-# device kernel measured 78% on this prefix.  The gate is that fp32 floor minus noise.
-SPIN_FRACTION_FP32_SK2000 = 0.70
+
+
+def fp32_floor_gate(k=None):
+    """Dense fp32 kernels on Gaussian SK N=2000, T up to 40: the committed fp32 replay of the
+    reference (tests/golden/cfg2_sk2000_f32replay.npz, oracle/mars_oracle.c
+    orc_replay_batch_f32: the same descents with fp32 state, fields and tanh) ends on the
+    reference's spins in 80.1% of the first 256 runs -- a chaotic descent split by rounding
+    reaches another local minimum.  Gate: that floor minus a 3-sigma binomial margin."""
+    g = golden("cfg2_sk2000_prefix")
+    r = golden("cfg2_sk2000_f32replay")
+    k = len(g["status"]) if k is None else k
+    floor = np.all(unpack_spins(r["spins_packed"], 2000)[:k] == unpack_spins(g["spins_packed"], 2000)[:k],
+                   axis=1).mean()
+    return floor - 3.0 * np.sqrt(floor * (1.0 - floor) / k)
+
+
+SPIN_FRACTION_FP32_SK2000 = fp32_floor_gate()
 
 
 def uniform(t_max, t_min=0.0):
@@ -230,10 +243,10 @@ def test_workload_prefix_matches_reference(name, frac):
         assert np.array_equal(rec.descent_iters[:k], g["iters"][:k])
         assert compare_records(rec, g, w.n, frac=1.0) == 1.0
     assert abs(p.coupling_sum() - g["coupling_sum"][0]) == 0.0
-    # the device's best over the prefix is within 0.5% of the reference's
+    # the device's best over the prefix is equal to or better than the reference's
     dev_best = rec.energy[rec.status == 0].min()
     ref_best = g["energy"][g["status"] == 0].min()
-    assert dev_best <= ref_best + 5e-3 * abs(ref_best)
+    assert dev_best <= ref_best + (0.0 if p.integral() else 1e-9), (dev_best, ref_best)
 
 
 @pytest.mark.parametrize("kind", ["ea2d", "ea3d", "er_gauss"])

