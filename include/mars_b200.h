@@ -191,6 +191,34 @@ int mars_batch_fetch(mars_batch_t* b, mars_records_t* records, int64_t* best_ind
 int mars_batch_fetch_finish(mars_batch_t* b, double* finish_seconds);
 void mars_batch_destroy(mars_batch_t* b);
 
+/* ---- the synchronous mean-field baselines (solvers.hpp:62-82, 154-158) ------------------
+ *
+ * run_batch with NmfaParams / SimCimParams (runner.cpp:31-60: run index k uses the stream
+ * Rng(sub_seed(base_seed, k))): every run on the tcgen05 Jacobi kernel (one GEMM per
+ * iteration, update + the run's Box-Muller noise fused into the epilogue), exact energies,
+ * best-of-R and the reference's aggregation.  Same validation and messages as
+ * validate(NmfaParams) / validate(SimCimParams).  The schedule is stretched over `iters` like
+ * schedule_at (solvers.cpp:118-123); records.start_temp = schedule[0], descent_iters = iters. */
+typedef struct {
+    double noise_sigma;          /* NmfaParams::noise_sigma (0.15)                          */
+    double alpha;                /* NmfaParams::alpha (0.15), in (0, 1]                     */
+    int64_t iters;
+    const double* schedule;      /* temperatures, >= 0 (nmfa_defaults: 2.0 -> 0.02, 64)    */
+    int64_t schedule_len;
+} mars_nmfa_params_t;
+typedef struct {
+    double step_size;            /* SimCimParams::step_size (0.1)                           */
+    double noise_sigma;          /* SimCimParams::noise_sigma (0.03)                        */
+    int64_t iters;
+    const double* pump_schedule; /* simcim_defaults: -2.0 -> 1.0, 64 points                 */
+    int64_t pump_schedule_len;
+} mars_simcim_params_t;
+int mars_run_batch_nmfa(mars_problem_t* p, const mars_nmfa_params_t* prm, int64_t runs, uint64_t base_seed,
+                        mars_records_t* records, mars_stats_t* stats, int8_t* best_spins);
+int mars_run_batch_simcim(mars_problem_t* p, const mars_simcim_params_t* prm, int64_t runs,
+                          uint64_t base_seed, mars_records_t* records, mars_stats_t* stats,
+                          int8_t* best_spins);
+
 /* ---- TEST-ONLY hook: single sweeps through the device kernels -------------------------
  *
  * mars_relax_sweep (solvers.cpp:150-161) from caller-given states: for each of `count`
@@ -202,6 +230,11 @@ void mars_batch_destroy(mars_batch_t* b);
  * Exists so the tests can pin one sweep of the device path against the reference. */
 int mars_debug_sweeps(mars_problem_t* p, int64_t count, const float* s_in, const double* temps,
                       int32_t sweeps, float* s_out, int32_t* kernel_used);
+
+/* TEST-ONLY: the device copy of Rng(seed) (mt_device.cuh) for `streams` seeds: the first
+ * `count` engine outputs and, from a second copy of the stream, the first `count` gaussian()
+ * draws (rng.hpp:27-75), row per stream. */
+int mars_debug_rng(const uint64_t* seeds, int32_t streams, int32_t count, uint64_t* u64, double* gauss);
 
 /* ---- instance generators built from the reference Rng --------------- */
 void mars_gen_sk_gaussian(int32_t n, uint64_t seed, double* J);     /* io.cpp:151-163 */

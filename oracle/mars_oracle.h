@@ -95,6 +95,13 @@ ORC_DECLARE(orc_)
 
 /* port-only test knob: override kMarsSweepCap (0 restores 10^6) */
 void orc_set_sweep_cap(int64_t cap);
+/* TEST-ONLY (ref_driver.cpp, reference only): run_batch with NmfaParams / SimCimParams. */
+int ref_run_batch_nmfa(const void* p, double noise_sigma, double alpha, int64_t iters, const double* sched,
+                       int64_t sched_len, int64_t runs, uint64_t base_seed, int workers, orc_records_t* rec,
+                       orc_stats_t* st, char* err, int errlen);
+int ref_run_batch_simcim(const void* p, double step_size, double noise_sigma, int64_t iters, const double* sched,
+                         int64_t sched_len, int64_t runs, uint64_t base_seed, int workers, orc_records_t* rec,
+                         orc_stats_t* st, char* err, int errlen);
 /* TEST-ONLY measurement tool (mars_oracle.c): the reference descent replayed in fp32
  * (mode 0) or fp32 with J rounded to one fp16 plane (mode 1); dense problems only. */
 double orc_relax_sweep_f32(const void* p, float* s, double t);

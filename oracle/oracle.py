@@ -112,6 +112,14 @@ class Oracle:
         self._gen_pm1 = f("gen_sk_pm1", None, i32, u64, vp)
         self._gen_er = f("gen_er", i64, i32, dbl, u64, vp, vp, vp)
         self._gen_ea = f("gen_ea", i64, i32, i32, u64, vp, vp, vp)
+        if kind == "ref":
+            for nm in ("ref_run_batch_nmfa", "ref_run_batch_simcim"):
+                fn = getattr(L, nm)
+                fn.restype = i32
+                fn.argtypes = [vp, dbl, dbl, i64, vp, i64, i64, u64, i32, C.POINTER(OracleRecords),
+                               C.POINTER(OracleStats), C.c_char_p, i32]
+            self._nmfa = L.ref_run_batch_nmfa
+            self._simcim = L.ref_run_batch_simcim
         if kind == "port":
             self._sweep32 = L.orc_relax_sweep_f32
             self._sweep32.restype = dbl
@@ -275,6 +283,27 @@ class OracleProblem:
         """Port only (TEST-ONLY): one in-order sweep in fp32 (the fp32 floor), in place."""
         assert s.dtype == np.float32 and s.flags.c_contiguous
         return self.orc._sweep32(self.h, _ptr(s), t)
+
+    def run_sync(self, solver: str, a: float, b: float, iters: int, schedule, runs: int, base_seed: int,
+                 workers: int = 0) -> OracleBatch:
+        """Reference only: run_batch with NmfaParams (a = noise_sigma, b = alpha) or SimCimParams
+        (a = step_size, b = noise_sigma) -- the checker of the device's synchronous baselines."""
+        sched = np.ascontiguousarray(schedule, np.float64)
+        status = np.zeros(runs, np.uint8)
+        energy, cut = np.zeros(runs), np.zeros(runs)
+        t0, el = np.zeros(runs), np.zeros(runs)
+        iters_out = np.zeros(runs, np.int64)
+        sp = np.zeros((runs, self.n), np.int8)
+        rec = OracleRecords(_ptr(status), _ptr(energy), _ptr(cut), _ptr(t0), _ptr(iters_out), _ptr(el), _ptr(sp))
+        st = OracleStats()
+        err = C.create_string_buffer(256)
+        fn = self.orc._nmfa if solver == "nmfa" else self.orc._simcim
+        rc = fn(self.h, a, b, iters, _ptr(sched), len(sched), runs, base_seed, workers, C.byref(rec),
+                C.byref(st), err, 256)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        stats = {k: getattr(st, k) for k, _ in OracleStats._fields_}
+        return OracleBatch(status, energy, cut, t0, iters_out, el, sp, stats)
 
     def replay_f32(self, prm: OracleParams, runs: int, base_seed: int, workers: int = 0, mode: int = 0):
         """Port only (TEST-ONLY measurement tool): the first `runs` descents replayed with fp32

@@ -197,6 +197,43 @@ int ref_descent(const void* p, double start_temp, const orc_params_t* prm, uint6
     }
 }
 
+namespace {
+// BatchStats -> the C records / stats (index order; best_result = first strict minimum)
+void fill_batch(const mars::IsingProblem& prob, const mars::BatchStats& s, orc_records_t* rec, orc_stats_t* st) {
+    const int n = prob.size();
+    int64_t best_index = -1;
+    for (std::size_t k = 0; k < s.runs.size(); ++k) {
+        const mars::RunResult& r = s.runs[k];
+        if (rec) {
+            if (rec->status) rec->status[k] = static_cast<uint8_t>(r.status);
+            if (rec->energy) rec->energy[k] = r.energy;
+            if (rec->cut) rec->cut[k] = r.cut;
+            if (rec->start_temp) rec->start_temp[k] = r.start_temp;
+            if (rec->descent_iters) rec->descent_iters[k] = r.descent_iters;
+            if (rec->elapsed_seconds) rec->elapsed_seconds[k] = r.elapsed_seconds;
+            if (rec->spins && r.spins.size() == static_cast<std::size_t>(n))
+                std::memcpy(rec->spins + k * static_cast<std::size_t>(n), r.spins.data(),
+                            static_cast<std::size_t>(n));
+        }
+        // best_result is the first strict minimum (runner.cpp:147-150)
+        if (best_index < 0 && r.status == mars::RunStatus::Ok && r.energy == s.best_energy)
+            best_index = static_cast<int64_t>(k);
+    }
+    st->best_energy = s.best_energy;
+    st->mean_energy = s.mean_energy;
+    st->best_cut = s.best_cut;
+    st->mean_cut = s.mean_cut;
+    st->hit_count = s.hit_count;
+    st->success_probability = s.success_probability;
+    st->total_seconds = s.total_seconds;
+    st->mean_seconds_per_run = s.mean_seconds_per_run;
+    st->best_index = best_index;
+    st->completed_runs = s.completed_runs;
+    st->skipped_runs = s.skipped_runs;
+    st->failed_runs = s.failed_runs;
+}
+}  // namespace
+
 int ref_run_batch(const void* p, const orc_params_t* prm, int64_t runs, uint64_t base_seed,
                   int workers, orc_records_t* rec, orc_stats_t* st, char* err, int errlen) {
     try {
@@ -206,37 +243,7 @@ int ref_run_batch(const void* p, const orc_params_t* prm, int64_t runs, uint64_t
         spec.base_seed = base_seed;
         spec.workers = workers;
         const mars::BatchStats s = mars::run_batch(P(p), spec);                    // runner.cpp:170
-        const int n = P(p).size();
-        int64_t best_index = -1;
-        for (std::size_t k = 0; k < s.runs.size(); ++k) {
-            const mars::RunResult& r = s.runs[k];
-            if (rec) {
-                if (rec->status) rec->status[k] = static_cast<uint8_t>(r.status);
-                if (rec->energy) rec->energy[k] = r.energy;
-                if (rec->cut) rec->cut[k] = r.cut;
-                if (rec->start_temp) rec->start_temp[k] = r.start_temp;
-                if (rec->descent_iters) rec->descent_iters[k] = r.descent_iters;
-                if (rec->elapsed_seconds) rec->elapsed_seconds[k] = r.elapsed_seconds;
-                if (rec->spins && r.spins.size() == static_cast<std::size_t>(n))
-                    std::memcpy(rec->spins + k * static_cast<std::size_t>(n), r.spins.data(),
-                                static_cast<std::size_t>(n));
-            }
-            // best_result is the first strict minimum (runner.cpp:147-150)
-            if (best_index < 0 && r.status == mars::RunStatus::Ok && r.energy == s.best_energy)
-                best_index = static_cast<int64_t>(k);
-        }
-        st->best_energy = s.best_energy;
-        st->mean_energy = s.mean_energy;
-        st->best_cut = s.best_cut;
-        st->mean_cut = s.mean_cut;
-        st->hit_count = s.hit_count;
-        st->success_probability = s.success_probability;
-        st->total_seconds = s.total_seconds;
-        st->mean_seconds_per_run = s.mean_seconds_per_run;
-        st->best_index = best_index;
-        st->completed_runs = s.completed_runs;
-        st->skipped_runs = s.skipped_runs;
-        st->failed_runs = s.failed_runs;
+        fill_batch(P(p), s, rec, st);
         return 0;
     } catch (const mars::InputError& e) {
         put_err(err, errlen, e.what());
@@ -308,6 +315,56 @@ int64_t ref_gen_ea(int L, int dims, uint64_t seed, int32_t* u, int32_t* v, doubl
         }
     }
     return m;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// TEST-ONLY: the reference's run_batch with NmfaParams / SimCimParams (runner.cpp:31-60,
+// solvers.cpp:374-443) -- the checker for the device's synchronous baselines.
+int ref_run_batch_nmfa(const void* p, double noise_sigma, double alpha, int64_t iters, const double* sched,
+                       int64_t sched_len, int64_t runs, uint64_t base_seed, int workers, orc_records_t* rec,
+                       orc_stats_t* st, char* err, int errlen) {
+    try {
+        mars::NmfaParams np;
+        np.noise_sigma = noise_sigma;
+        np.alpha = alpha;
+        np.iters = iters;
+        np.schedule.assign(sched, sched + sched_len);
+        mars::BatchSpec spec;
+        spec.params = np;
+        spec.runs = runs;
+        spec.base_seed = base_seed;
+        spec.workers = workers;
+        fill_batch(P(p), mars::run_batch(P(p), spec), rec, st);
+        return 0;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return 1;
+    }
+}
+
+int ref_run_batch_simcim(const void* p, double step_size, double noise_sigma, int64_t iters, const double* sched,
+                         int64_t sched_len, int64_t runs, uint64_t base_seed, int workers, orc_records_t* rec,
+                         orc_stats_t* st, char* err, int errlen) {
+    try {
+        mars::SimCimParams sp;
+        sp.step_size = step_size;
+        sp.noise_sigma = noise_sigma;
+        sp.iters = iters;
+        sp.pump_schedule.assign(sched, sched + sched_len);
+        mars::BatchSpec spec;
+        spec.params = sp;
+        spec.runs = runs;
+        spec.base_seed = base_seed;
+        spec.workers = workers;
+        fill_batch(P(p), mars::run_batch(P(p), spec), rec, st);
+        return 0;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return 1;
+    }
 }
 
 }  // extern "C"

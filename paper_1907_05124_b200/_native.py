@@ -55,6 +55,16 @@ class mars_timing_t(C.Structure):
                 ("grid", C.c_int32), ("slots", C.c_int32), ("kernel", C.c_int32), ("reserved", C.c_int32)]
 
 
+class mars_nmfa_params_t(C.Structure):
+    _fields_ = [("noise_sigma", C.c_double), ("alpha", C.c_double), ("iters", C.c_int64),
+                ("schedule", C.c_void_p), ("schedule_len", C.c_int64)]
+
+
+class mars_simcim_params_t(C.Structure):
+    _fields_ = [("step_size", C.c_double), ("noise_sigma", C.c_double), ("iters", C.c_int64),
+                ("pump_schedule", C.c_void_p), ("pump_schedule_len", C.c_int64)]
+
+
 vp, i32, i64, u64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double
 P_params = C.POINTER(mars_params_t)
 
@@ -85,6 +95,9 @@ SIGNATURES = {
     "mars_batch_upload": (C.c_int, [vp]),
     "mars_batch_execute": (C.c_int, [vp, C.POINTER(mars_timing_t)]),
     "mars_debug_sweeps": (C.c_int, [vp, i64, vp, vp, i32, vp, vp]),
+    "mars_debug_rng": (C.c_int, [vp, i32, i32, vp, vp]),
+    "mars_run_batch_nmfa": (C.c_int, [vp, C.POINTER(mars_nmfa_params_t), i64, u64, vp, vp, vp]),
+    "mars_run_batch_simcim": (C.c_int, [vp, C.POINTER(mars_simcim_params_t), i64, u64, vp, vp, vp]),
     "mars_batch_fetch": (C.c_int, [vp, C.POINTER(mars_records_t), vp, vp]),
     "mars_batch_fetch_finish": (C.c_int, [vp, vp]),
     "mars_batch_destroy": (None, [vp]),

@@ -47,6 +47,8 @@ struct RelaxArgs {
     // ([count][n] fp32) -- the device counterpart of mars_relax_sweep (solvers.cpp:150-161)
     int fixed_sweeps;
     float* state_out;
+    // tcgen05 kernel: the field GEMM runs on J * 2^k (fp16 range); fields scale back by 2^-k
+    float jscale;
 };
 constexpr int kProfSlots = 16;
 
@@ -95,6 +97,44 @@ int relax_dense_umma_block();
 int relax_dense_umma_kc();      // K per pipeline stage (the TMA box width of both operand maps)
 int relax_dense_umma_j_rows();  // coupling-tile rows per CTA of the pair (TMA box height of J maps)
 std::size_t relax_dense_umma_plane_rows(int grid);
+
+// Synchronous mean-field baselines on tcgen05 (jacobi_umma.cu): NMFA (solver 0) and SimCIM
+// (solver 1), solvers.cpp:374-443.  CTA pairs (grid even); 128 runs per CTA per tile round.
+struct JacobiArgs {
+    int n, np;
+    int solver;                // 0 = NMFA, 1 = SimCIM
+    int iters;
+    const double* sched;       // [iters] schedule_at(...) per iteration: temperature / pump
+    double noise_sigma;
+    float alpha_f, one_minus_alpha_f, step_f;
+    float jscale;              // 2^-k: the GEMM runs on J * 2^k (fp16 range)
+    const float* norm;         // [np] NMFA normalisers sqrt(h_i^2 + sum_j J_ij^2) (fp32)
+    const float* h32;          // [np] field or nullptr
+    int queue_len;
+    int* queue_head;
+    const int* order;          // [queue_len] run index
+    const std::uint64_t* seeds;   // [count] per-run rng seed (sub_seed(base, index))
+    std::uint64_t* mt;         // [312][slots] mt19937_64 states (word-major)
+    int slots;
+    __half* s_hi[2];           // state double buffer, fp16 hi/lo planes [slots][np]
+    __half* s_lo[2];
+    std::uint8_t* status;
+    long long* iters_out;
+    double* elapsed;
+    unsigned long long* done_ns;
+    std::int8_t* spins;        // [count][n]
+    float* state_out;          // TEST-ONLY final states [count][n] fp32, or nullptr
+};
+struct JacobiLaunch {
+    CUtensorMap tm_s[2][2];    // [buffer][hi, lo]
+    CUtensorMap tm_jhi, tm_jlo;
+    bool jlo;
+};
+cudaError_t launch_jacobi_umma(const JacobiArgs& a, const JacobiLaunch& l, int grid, cudaStream_t st);
+constexpr int kMtWords = 312;   // mt19937_64 state words per run slot (mt_device.cuh)
+cudaError_t launch_rng_probe(const std::uint64_t* seeds, int streams, int count, std::uint64_t* st,
+                             std::uint64_t* u64, double* gauss, cudaStream_t s);
+int jacobi_umma_slots_per_cta();
 
 // Level-scheduled sparse kernel (relax_csr.cu).  Spins grouped by Gauss-Seidel level,
 // levels cut into cw-spin chunks, each chunk's neighbour lists interleaved [k][cw].

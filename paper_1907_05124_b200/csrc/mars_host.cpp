@@ -146,10 +146,13 @@ struct mars_problem {
     double* dWblk = nullptr;
     float* dH32 = nullptr;
     double* dH64 = nullptr;
-    __half* dJhi = nullptr;         // [np][np] fp16 split of J (tcgen05 kernel)
+    __half* dJhi = nullptr;         // [np][np] fp16 split of J * 2^jexp (tcgen05 kernels)
     __half* dJlo = nullptr;
     bool jlo = true;                // J_lo nonzero somewhere (non-integer couplings)
+    int jexp = 0;                   // power-of-two prescale of the fp16 planes
+    int np16 = 0;                   // padded size of the fp16 planes (multiple of 128)
     CUtensorMap tm_jhi{}, tm_jlo{};
+    float* dNorm = nullptr;         // NMFA normalisers (lazily, fp32 [np16])
     // Buffer pool for the batches run on this problem: repeated run_batch calls reuse their
     // pinned host and device allocations (a 65536 x 2000 fp64 plan is 1 GB pinned) instead of
     // allocating and freeing them every call.
@@ -191,6 +194,7 @@ struct mars_problem {
         }
         cudaFree(dJhi);
         cudaFree(dJlo);
+        cudaFree(dNorm);
         cudaSetDevice(device);
         cudaFree(dJ32);
         cudaFree(dJ64);
@@ -422,6 +426,46 @@ int build_levels(mars_problem* p, const std::vector<int>& off, const std::vector
     return MARS_OK;
 }
 
+// fp16 split operand planes of the tcgen05 kernels: J * 2^jexp = J_hi + J_lo, [np16][np16],
+// zero padded, plus their TMA maps.  The power-of-two prescale keeps every coupling inside
+// fp16's range (|J_hi| < 2^14) and J_lo out of fp16 subnormals for the bulk of the couplings;
+// it is exact, and the kernels scale the fp32 GEMM fields back by 2^-jexp.  Integer couplings
+// up to 2048 are exact in J_hi unscaled (no J_lo product, integer fields stay exact).
+int build_umma_planes(mars_problem* p) {
+    if (p->dJhi) return MARS_OK;
+    const int n = p->n;
+    p->np16 = round_up(n, relax_dense_umma_block());
+    const int np = p->np16;
+    std::vector<double> w(static_cast<std::size_t>(np) * np, 0.0);
+    double jmax = 0.0;
+    if (p->dense) {
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) w[static_cast<std::size_t>(i) * np + j] = p->J[static_cast<std::size_t>(i) * n + j];
+    } else {
+        for (int i = 0; i < n; ++i)
+            for (int k = p->off[i]; k < p->off[i + 1]; ++k) w[static_cast<std::size_t>(i) * np + p->idx[k]] += p->wt[k];
+    }
+    for (double v : w) jmax = std::max(jmax, std::fabs(v));
+    p->jexp = 0;
+    if (!(p->integral && jmax <= 2048.0) && jmax > 0.0)
+        p->jexp = std::max(-120, std::min(120, 13 - static_cast<int>(std::floor(std::log2(jmax)))));
+    const double sc = std::ldexp(1.0, p->jexp);
+    std::vector<__half> jh(w.size()), jl(w.size());
+    p->jlo = false;
+    for (std::size_t k = 0; k < w.size(); ++k) {
+        const double v = w[k] * sc;
+        jh[k] = __double2half(v);
+        jl[k] = __double2half(v - static_cast<double>(__half2float(jh[k])));
+        if (__half2float(jl[k]) != 0.0f) p->jlo = true;
+    }
+    if (int rc = upload(&p->dJhi, jh.data(), jh.size())) return rc;
+    if (int rc = upload(&p->dJlo, jl.data(), jl.size())) return rc;
+    if (!make_tmap_f16(&p->tm_jhi, p->dJhi, np, np, relax_dense_umma_kc(), relax_dense_umma_j_rows()) ||
+        !make_tmap_f16(&p->tm_jlo, p->dJlo, np, np, relax_dense_umma_kc(), relax_dense_umma_j_rows()))
+        return fail(MARS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the coupling planes");
+    return MARS_OK;
+}
+
 // Device copies in the layouts the kernels use.
 int build_device_store(mars_problem* p) {
     int ndev = 0;
@@ -462,26 +506,8 @@ int build_device_store(mars_problem* p) {
                     j32[static_cast<std::size_t>(i) * p->np + p->idx[k]] += static_cast<float>(p->wt[k]);
         }
         if (int rc = upload(&p->dJ32, j32.data(), j32.size())) return rc;
-        if (p->kernel == MARS_KERNEL_DENSE_UMMA) {
-            // fp16 split J = J_hi + J_lo (the tensor-core operand planes)
-            std::vector<__half> jh(j32.size()), jl(j32.size());
-            p->jlo = false;
-            for (std::size_t k = 0; k < j32.size(); ++k) {
-                const int i = static_cast<int>(k / p->np), j = static_cast<int>(k % p->np);
-                const double w = (i < n && j < n)
-                                     ? (p->dense ? p->J[static_cast<std::size_t>(i) * n + j] : static_cast<double>(j32[k]))
-                                     : 0.0;
-                jh[k] = __double2half(w);
-                jl[k] = __double2half(w - static_cast<double>(__half2float(jh[k])));
-                if (__half2float(jl[k]) != 0.0f) p->jlo = true;
-            }
-            if (int rc = upload(&p->dJhi, jh.data(), jh.size())) return rc;
-            if (int rc = upload(&p->dJlo, jl.data(), jl.size())) return rc;
-            const int tb = relax_dense_umma_block();
-            if (!make_tmap_f16(&p->tm_jhi, p->dJhi, p->np, p->np, relax_dense_umma_kc(), relax_dense_umma_j_rows()) ||
-                !make_tmap_f16(&p->tm_jlo, p->dJlo, p->np, p->np, relax_dense_umma_kc(), relax_dense_umma_j_rows()))
-                return fail(MARS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the coupling planes");
-        }
+        if (p->kernel == MARS_KERNEL_DENSE_UMMA)
+            if (int rc = build_umma_planes(p)) return rc;
     } else {
         // relaxation CSR: the reference's sorted adjacency, or the nonzeros of a dense store in
         // ascending columns (row_dot order minus zero terms, which add nothing: acc is never -0)
@@ -763,7 +789,7 @@ int batch_alloc(mars_batch* b) {
         // 1024 runs 16.0K vs 12.5K, 2368: 34.4K vs 29.1K, 4736: 69K vs 58K, 9472: 104K vs
         // 93K, 18944: 139K vs 183K -- so up to 4 x 16 warps x SMs runs.
         // MARS_DENSE_SMALL=1 forces it (when eligible), =0 forbids it.
-        const bool small_ok = !p->jlo && p->n <= relax_small_max_n();
+        const bool small_ok = !p->jlo && p->jexp == 0 && p->n <= relax_small_max_n();
         const int small_env = env_int("MARS_DENSE_SMALL", -1);
         const std::int64_t small_max_runs = static_cast<std::int64_t>(4) * relax_small_slots_per_cta() * p->num_sms;
         b->use_small = small_ok && (small_env == 1 || (small_env < 0 && b->queue_len <= small_max_runs));
@@ -1219,6 +1245,7 @@ int execute_impl(mars_batch_t* b, mars_timing_t* timing, int fixed_sweeps, float
     ra.done_ns = b->d_done;
     ra.spins = b->d_spins;
     ra.fixed_sweeps = fixed_sweeps;
+    ra.jscale = static_cast<float>(std::ldexp(1.0, -p->jexp));
     ra.state_out = d_state_out;
     std::int64_t launches = 0;
     const bool prof = std::getenv("MARS_PROFILE") != nullptr;
@@ -1532,6 +1559,232 @@ int mars_run_batch(mars_problem_t* p, const mars_params_t* prm, int64_t runs, ui
                                           " disagrees with the host aggregation " +
                                           std::to_string(stats->best_index));
     return MARS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// schedule_at (solvers.cpp:118-123): the stored sequence stretched / compressed by index
+double schedule_at(const double* sched, std::int64_t len, std::int64_t k, std::int64_t iters) {
+    if (len == iters) return sched[k];
+    const std::int64_t idx = std::min(len - 1, k * len / iters);
+    return sched[idx];
+}
+
+// Device-owning scratch of one synchronous-solver batch.
+struct JacobiScratch {
+    std::vector<void*> bufs;
+    ~JacobiScratch() {
+        for (void* b : bufs) cudaFree(b);
+    }
+    template <class T>
+    int alloc(T** p, std::size_t count) {
+        void* q = nullptr;
+        CUDA_TRY(cudaMalloc(&q, std::max<std::size_t>(count, 1) * sizeof(T)));
+        bufs.push_back(q);
+        *p = static_cast<T*>(q);
+        return MARS_OK;
+    }
+};
+
+// run_batch for NmfaParams / SimCimParams (runner.cpp:31-60, 81-178): every run index through
+// the tcgen05 Jacobi kernel, exact energies, best-of-R, then the reference's aggregation.
+int run_jacobi(mars_problem* p, int solver, std::int64_t iters, const double* sched, std::int64_t sched_len,
+               double alpha, double noise_sigma, double step_size, std::int64_t runs, std::uint64_t base_seed,
+               mars_records_t* records, mars_stats_t* stats, std::int8_t* best_spins) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (runs < 1) return fail(MARS_ERR_INPUT, "batch needs runs >= 1");            // effective_runs
+    if (runs > (1 << 30)) return fail(MARS_ERR_INPUT, "batch too large");
+    CUDA_TRY(cudaSetDevice(p->device));
+    if (int rc = build_umma_planes(p)) return rc;
+    const int n = p->n, np = p->np16;
+    cudaStream_t st = p->stream;
+    if (solver == 0 && !p->dNorm) {
+        // nmfa_normalizers (solvers.cpp:364-372): sqrt(h_i^2 + row_sumsq(i)), row_sumsq in the
+        // storage order of model.cpp:165-175
+        std::vector<float> nrm(np, 0.0f);
+        for (int i = 0; i < n; ++i) {
+            double acc = 0.0;
+            if (p->dense) {
+                const double* row = p->J.data() + static_cast<std::size_t>(i) * n;
+                for (int j = 0; j < n; ++j) acc += row[j] * row[j];
+            } else {
+                for (int k = p->off[i]; k < p->off[i + 1]; ++k) acc += p->wt[k] * p->wt[k];
+            }
+            nrm[i] = static_cast<float>(std::sqrt(p->h[i] * p->h[i] + acc));
+        }
+        if (int rc = upload(&p->dNorm, nrm.data(), nrm.size())) return rc;
+    }
+    const int count = static_cast<int>(runs);
+    const int tm = jacobi_umma_slots_per_cta();
+    int grid = std::min((count + tm - 1) / tm, p->num_sms & ~1);
+    grid = std::max(2, grid + (grid & 1));
+    const int slots = grid * tm;
+    JacobiScratch sc;
+    JacobiArgs a{};
+    a.n = n;
+    a.np = np;
+    a.solver = solver;
+    a.iters = static_cast<int>(iters);
+    a.noise_sigma = noise_sigma;
+    a.alpha_f = static_cast<float>(alpha);
+    a.one_minus_alpha_f = static_cast<float>(1.0 - alpha);
+    a.step_f = static_cast<float>(step_size);
+    a.jscale = static_cast<float>(std::ldexp(1.0, -p->jexp));
+    a.norm = p->dNorm;
+    a.h32 = p->dH32;
+    a.queue_len = count;
+    a.slots = slots;
+    std::vector<double> sv(static_cast<std::size_t>(iters));
+    for (std::int64_t k = 0; k < iters; ++k) sv[k] = schedule_at(sched, sched_len, k, iters);
+    std::vector<std::uint64_t> seeds(count);
+    std::vector<int> order(count);
+    for (int k = 0; k < count; ++k) {
+        seeds[k] = sub_seed(base_seed, static_cast<std::uint64_t>(k));           // runner.cpp:55
+        order[k] = k;
+    }
+    double *d_sched, *d_elapsed, *d_energy, *d_cut, *d_part_e;
+    std::uint64_t *d_seeds, *d_mt;
+    int *d_order, *d_queue;
+    std::uint8_t* d_status;
+    long long *d_iters, *d_part_i, *d_best;
+    unsigned long long* d_done;
+    std::int8_t* d_spins;
+    __half* planes[4];
+    const int best_grid = std::max(1, std::min((count + 255) / 256, 2 * p->num_sms));
+    for (auto& pl : planes)
+        if (int rc = sc.alloc(&pl, static_cast<std::size_t>(slots) * np)) return rc;
+    if (int rc = sc.alloc(&d_sched, sv.size())) return rc;
+    if (int rc = sc.alloc(&d_seeds, seeds.size())) return rc;
+    if (int rc = sc.alloc(&d_order, order.size())) return rc;
+    if (int rc = sc.alloc(&d_queue, 1)) return rc;
+    if (int rc = sc.alloc(&d_mt, static_cast<std::size_t>(kMtWords) * slots)) return rc;
+    if (int rc = sc.alloc(&d_status, count)) return rc;
+    if (int rc = sc.alloc(&d_iters, count)) return rc;
+    if (int rc = sc.alloc(&d_elapsed, count)) return rc;
+    if (int rc = sc.alloc(&d_done, count)) return rc;
+    if (int rc = sc.alloc(&d_spins, static_cast<std::size_t>(count) * n)) return rc;
+    if (int rc = sc.alloc(&d_energy, count)) return rc;
+    if (int rc = sc.alloc(&d_cut, count)) return rc;
+    if (int rc = sc.alloc(&d_part_e, best_grid)) return rc;
+    if (int rc = sc.alloc(&d_part_i, best_grid)) return rc;
+    if (int rc = sc.alloc(&d_best, 1)) return rc;
+    CUDA_TRY(cudaMemcpyAsync(d_sched, sv.data(), sv.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(d_seeds, seeds.data(), seeds.size() * sizeof(std::uint64_t), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(d_order, order.data(), order.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(d_queue, 0, sizeof(int), st));
+    CUDA_TRY(cudaMemsetAsync(d_status, 255, count, st));
+    a.sched = d_sched;
+    a.seeds = d_seeds;
+    a.order = d_order;
+    a.queue_head = d_queue;
+    a.mt = d_mt;
+    a.s_hi[0] = planes[0];
+    a.s_lo[0] = planes[1];
+    a.s_hi[1] = planes[2];
+    a.s_lo[1] = planes[3];
+    a.status = d_status;
+    a.iters_out = d_iters;
+    a.elapsed = d_elapsed;
+    a.done_ns = d_done;
+    a.spins = d_spins;
+    a.state_out = nullptr;
+    JacobiLaunch l{};
+    for (int bsel = 0; bsel < 2; ++bsel)
+        for (int pl = 0; pl < 2; ++pl)
+            if (!make_tmap_f16(&l.tm_s[bsel][pl], planes[2 * bsel + pl], slots, np, relax_dense_umma_kc(), tm))
+                return fail(MARS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the state planes");
+    l.tm_jhi = p->tm_jhi;
+    l.tm_jlo = p->tm_jlo;
+    l.jlo = p->jlo;
+    CUDA_TRY(launch_jacobi_umma(a, l, grid, st));
+    EnergyArgs ea{n, p->dJ64, p->dOff, p->dIdx, p->dW64, p->dH64, p->coupling_sum,
+                  count, d_spins, d_status, d_energy, d_cut};
+    CUDA_TRY(launch_energy(ea, st));
+    BestArgs ba{count, d_status, d_energy, d_part_e, d_part_i, d_best};
+    CUDA_TRY(launch_best(ba, best_grid, st));
+    std::vector<std::uint8_t> status(count);
+    std::vector<double> energy(count), cut(count), elapsed(count);
+    long long best = -1;
+    CUDA_TRY(cudaMemcpyAsync(status.data(), d_status, count, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(energy.data(), d_energy, count * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(cut.data(), d_cut, count * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(elapsed.data(), d_elapsed, count * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&best, d_best, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    if (records && records->spins)
+        CUDA_TRY(cudaMemcpyAsync(records->spins, d_spins, static_cast<std::size_t>(count) * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (int k = 0; k < count; ++k)
+        if (status[k] != MARS_RUN_OK) return fail(MARS_ERR_RUNTIME, "run " + std::to_string(k) + " did not complete");
+    if (best_spins && best >= 0)
+        CUDA_TRY(cudaMemcpy(best_spins, d_spins + static_cast<std::size_t>(best) * n, n, cudaMemcpyDeviceToHost));
+    if (records) {
+        if (records->status) std::copy(status.begin(), status.end(), records->status);
+        if (records->energy) std::copy(energy.begin(), energy.end(), records->energy);
+        if (records->cut) std::copy(cut.begin(), cut.end(), records->cut);
+        if (records->elapsed_seconds) std::copy(elapsed.begin(), elapsed.end(), records->elapsed_seconds);
+        if (records->start_temp) std::fill(records->start_temp, records->start_temp + count, sched[0]);
+        if (records->descent_iters) std::fill(records->descent_iters, records->descent_iters + count, iters);
+    }
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (int rc = mars_aggregate(count, status.data(), energy.data(), cut.data(), elapsed.data(),
+                                p->integral ? 0.0 : 1e-9, secs, stats))
+        return rc;
+    if (stats->best_index != best)
+        return fail(MARS_ERR_RUNTIME, "device best-of-R index disagrees with the host aggregation");
+    return MARS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+// TEST-ONLY (include/mars_b200.h): the device copy of the reference's stream
+int mars_debug_rng(const uint64_t* seeds, int32_t streams, int32_t count, uint64_t* u64, double* gauss) {
+    if (!seeds || !u64 || !gauss || streams < 1 || count < 1) return fail(MARS_ERR_INPUT, "bad argument");
+    JacobiScratch sc;
+    std::uint64_t *d_seeds, *d_st, *d_u;
+    double* d_g;
+    if (int rc = sc.alloc(&d_seeds, streams)) return rc;
+    if (int rc = sc.alloc(&d_st, static_cast<std::size_t>(2) * kMtWords * streams)) return rc;
+    if (int rc = sc.alloc(&d_u, static_cast<std::size_t>(streams) * count)) return rc;
+    if (int rc = sc.alloc(&d_g, static_cast<std::size_t>(streams) * count)) return rc;
+    CUDA_TRY(cudaMemcpy(d_seeds, seeds, streams * sizeof(std::uint64_t), cudaMemcpyHostToDevice));
+    CUDA_TRY(launch_rng_probe(d_seeds, streams, count, d_st, d_u, d_g, nullptr));
+    CUDA_TRY(cudaMemcpy(u64, d_u, static_cast<std::size_t>(streams) * count * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(gauss, d_g, static_cast<std::size_t>(streams) * count * sizeof(double), cudaMemcpyDeviceToHost));
+    return MARS_OK;
+}
+
+// run_batch with NmfaParams (validate: solvers.cpp:89-96; run: solvers.cpp:392-408)
+int mars_run_batch_nmfa(mars_problem_t* p, const mars_nmfa_params_t* prm, int64_t runs, uint64_t base_seed,
+                        mars_records_t* records, mars_stats_t* stats, int8_t* best_spins) {
+    if (!p || !prm || !stats) return fail(MARS_ERR_INPUT, "null argument");
+    if (!(prm->alpha > 0.0 && prm->alpha <= 1.0)) return fail(MARS_ERR_INPUT, "nmfa: alpha must lie in (0,1]");
+    if (!(prm->noise_sigma >= 0.0)) return fail(MARS_ERR_INPUT, "nmfa: noise_sigma must be >= 0");
+    if (prm->iters < 1) return fail(MARS_ERR_INPUT, "nmfa: iters must be >= 1");
+    if (prm->schedule_len < 1 || !prm->schedule)
+        return fail(MARS_ERR_INPUT, "nmfa: temperature schedule must not be empty");
+    for (std::int64_t k = 0; k < prm->schedule_len; ++k)
+        if (!(prm->schedule[k] >= 0.0)) return fail(MARS_ERR_INPUT, "nmfa: schedule temperatures must be >= 0");
+    if (prm->iters > (1 << 30)) return fail(MARS_ERR_INPUT, "nmfa: iters too large");
+    return run_jacobi(p, 0, prm->iters, prm->schedule, prm->schedule_len, prm->alpha, prm->noise_sigma, 0.0, runs,
+                      base_seed, records, stats, best_spins);
+}
+
+// run_batch with SimCimParams (validate: solvers.cpp:98-103; run: solvers.cpp:426-443)
+int mars_run_batch_simcim(mars_problem_t* p, const mars_simcim_params_t* prm, int64_t runs, uint64_t base_seed,
+                          mars_records_t* records, mars_stats_t* stats, int8_t* best_spins) {
+    if (!p || !prm || !stats) return fail(MARS_ERR_INPUT, "null argument");
+    if (!(prm->step_size > 0.0)) return fail(MARS_ERR_INPUT, "simcim: step_size must be positive");
+    if (!(prm->noise_sigma >= 0.0)) return fail(MARS_ERR_INPUT, "simcim: noise_sigma must be >= 0");
+    if (prm->iters < 1) return fail(MARS_ERR_INPUT, "simcim: iters must be >= 1");
+    if (prm->pump_schedule_len < 1 || !prm->pump_schedule)
+        return fail(MARS_ERR_INPUT, "simcim: pump schedule must not be empty");
+    if (prm->iters > (1 << 30)) return fail(MARS_ERR_INPUT, "simcim: iters too large");
+    return run_jacobi(p, 1, prm->iters, prm->pump_schedule, prm->pump_schedule_len, 0.0, prm->noise_sigma,
+                      prm->step_size, runs, base_seed, records, stats, best_spins);
 }
 
 // brute_force_ground_state (model.cpp:296-324): exhaustive Gray-code scan on the device

@@ -642,10 +642,12 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     }
                     float pv[SB];
                     tmem_ld16(tacc + k0, pv);
+                    // raw GEMM fields (t < 2) are on the prescaled couplings; the helper's are not
+                    const float sc = t >= 2 ? 1.0f : a.jscale;
                     float2 pf[SB / 2];
 #pragma unroll
                     for (int j = 0; j < SB / 2; ++j) {
-                        pf[j] = make_float2(pv[2 * j] + an[j].x, pv[2 * j + 1] + an[j].y);
+                        pf[j] = make_float2(fmaf(pv[2 * j], sc, an[j].x), fmaf(pv[2 * j + 1], sc, an[j].y));
                         an[j] = make_float2(0.0f, 0.0f);
                     }
                     t0 = clock64();
@@ -758,7 +760,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         float pv[SB];
                         tmem_ld16(tacc + t * SB, pv);
 #pragma unroll
-                        for (int j = 0; j < SB / 2; ++j) pf[j] = make_float2(pv[2 * j], pv[2 * j + 1]);
+                        for (int j = 0; j < SB / 2; ++j) pf[j] = make_float2(pv[2 * j] * a.jscale, pv[2 * j + 1] * a.jscale);
                         // Deltas already final: sub-blocks 0 .. t-3
                         for (int u = 0; u + 3 <= t; ++u) {
                             float du[SB];

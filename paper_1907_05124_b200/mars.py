@@ -98,8 +98,93 @@ class MarsParams:
                                int(self.sweep_cap))
 
 
-def validate(params: MarsParams) -> None:
-    """validate(MarsParams) -- solvers.cpp:35-41; raises InputError."""
+# ------------------------------------- synchronous baselines (solvers.hpp:62-91)
+
+def linear_schedule(start: float, stop: float, points: int) -> list:
+    """linear_schedule (solvers.cpp:105-116): evenly spaced, both ends included."""
+    if points < 1:
+        raise InputError("schedule needs at least one point")
+    if points == 1:
+        return [float(start)]
+    return [start + (stop - start) * k / (points - 1) for k in range(points)]
+
+
+def schedule_at(schedule, k: int, iters: int) -> float:
+    """schedule_at (solvers.cpp:118-123): the sequence stretched / compressed by index."""
+    n = len(schedule)
+    if n == iters:
+        return float(schedule[k])
+    return float(schedule[min(n - 1, k * n // iters)])
+
+
+@dataclass
+class NmfaParams:
+    """solvers.hpp:62-67 -- noisy mean-field annealing (run on the GPU Jacobi kernel)."""
+    noise_sigma: float = 0.15
+    alpha: float = 0.15
+    schedule: list = field(default_factory=list)
+    iters: int = 1000
+
+    def _c(self):
+        self._sched = np.ascontiguousarray(self.schedule, np.float64)
+        return N.mars_nmfa_params_t(float(self.noise_sigma), float(self.alpha), int(self.iters),
+                                    ptr(self._sched) if len(self._sched) else None, len(self._sched))
+
+
+@dataclass
+class SimCimParams:
+    """solvers.hpp:74-79 -- simulated coherent Ising machine (run on the GPU Jacobi kernel)."""
+    step_size: float = 0.1
+    noise_sigma: float = 0.03
+    pump_schedule: list = field(default_factory=list)
+    iters: int = 1000
+
+    def _c(self):
+        self._sched = np.ascontiguousarray(self.pump_schedule, np.float64)
+        return N.mars_simcim_params_t(float(self.step_size), float(self.noise_sigma), int(self.iters),
+                                      ptr(self._sched) if len(self._sched) else None, len(self._sched))
+
+
+def nmfa_defaults(iters: int = 1000) -> NmfaParams:
+    """nmfa_defaults (solvers.cpp:125-132)."""
+    return NmfaParams(0.15, 0.15, linear_schedule(2.0, 0.02, 64), iters)
+
+
+def simcim_defaults(iters: int = 1000) -> SimCimParams:
+    """simcim_defaults (solvers.cpp:134-141)."""
+    return SimCimParams(0.1, 0.03, linear_schedule(-2.0, 1.0, 64), iters)
+
+
+def _validate_sync(params) -> None:
+    """validate(NmfaParams) / validate(SimCimParams) (solvers.cpp:89-103), same messages."""
+    if isinstance(params, NmfaParams):
+        if not (0.0 < params.alpha <= 1.0):
+            raise InputError("nmfa: alpha must lie in (0,1]")
+        if not (params.noise_sigma >= 0.0):
+            raise InputError("nmfa: noise_sigma must be >= 0")
+        if params.iters < 1:
+            raise InputError("nmfa: iters must be >= 1")
+        if len(params.schedule) == 0:
+            raise InputError("nmfa: temperature schedule must not be empty")
+        if any(not (t >= 0.0) for t in params.schedule):
+            raise InputError("nmfa: schedule temperatures must be >= 0")
+    else:
+        if not (params.step_size > 0.0):
+            raise InputError("simcim: step_size must be positive")
+        if not (params.noise_sigma >= 0.0):
+            raise InputError("simcim: noise_sigma must be >= 0")
+        if params.iters < 1:
+            raise InputError("simcim: iters must be >= 1")
+        if len(params.pump_schedule) == 0:
+            raise InputError("simcim: pump schedule must not be empty")
+
+
+def validate(params) -> None:
+    """validate(MarsParams) -- solvers.cpp:35-41 (or the NMFA / SimCIM validators); raises
+    InputError."""
+    if isinstance(params, (NmfaParams, SimCimParams)):
+        _validate_sync(params)
+        return
     _check(lib.mars_validate_params(C.byref(params._c())))
 
 
@@ -507,6 +592,11 @@ def run_batch(problem: IsingProblem, spec: BatchSpec, progress: Optional[Progres
     once per run index, in index order, after the batch (runs complete inside one kernel).
     """
     validate(spec.params)
+    if isinstance(spec.params, (NmfaParams, SimCimParams)):
+        stats = _run_sync_batch(problem, spec)
+        if progress is not None:
+            _replay_progress(stats, progress)
+        return stats
     runs = mars_run_count(spec.params, spec.runs)
     n = problem.size()
     dist = _dist()
@@ -526,11 +616,32 @@ def run_batch(problem: IsingProblem, spec: BatchSpec, progress: Optional[Progres
         stats = aggregate(rec, problem.energy_equality_tolerance(), st.total_seconds)
         stats.best_result.spins = best
     if progress is not None:
-        best_so_far = float("inf")
-        for k in range(runs):
-            if stats.records.status[k] == RunStatus.Ok:
-                best_so_far = min(best_so_far, float(stats.records.energy[k]))
-            progress(k, best_so_far)
+        _replay_progress(stats, progress)
+    return stats
+
+
+def _replay_progress(stats: "BatchStats", progress: ProgressFn) -> None:
+    best_so_far = float("inf")
+    for k in range(len(stats.records.status)):
+        if stats.records.status[k] == RunStatus.Ok:
+            best_so_far = min(best_so_far, float(stats.records.energy[k]))
+        progress(k, best_so_far)
+
+
+def _run_sync_batch(problem: IsingProblem, spec: BatchSpec) -> "BatchStats":
+    """run_batch for NmfaParams / SimCimParams on the GPU (mars_run_batch_nmfa/_simcim)."""
+    if spec.runs < 1:
+        raise InputError("batch needs runs >= 1")
+    n = problem.size()
+    rec = Records.empty(int(spec.runs), n, spec.keep_spins)
+    c = rec.c()
+    st = N.mars_stats_t()
+    best = np.zeros(n, np.int8)
+    prm = spec.params._c()
+    fn = lib.mars_run_batch_nmfa if isinstance(spec.params, NmfaParams) else lib.mars_run_batch_simcim
+    _check(fn(problem._h, C.byref(prm), int(spec.runs), int(spec.base_seed), C.byref(c), C.byref(st), ptr(best)))
+    stats = aggregate(rec, problem.energy_equality_tolerance(), st.total_seconds)
+    stats.best_result.spins = best
     return stats
 
 
