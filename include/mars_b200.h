@@ -25,7 +25,7 @@ enum {
     MARS_ERR_INPUT = 1,      /* mars::InputError (errors.hpp:16)                            */
     MARS_ERR_RUNTIME = 2,    /* mars::Error (errors.hpp:11)                                  */
     MARS_ERR_CUDA = 3,       /* CUDA runtime failure or no device                            */
-    MARS_ERR_NCCL = 4,       /* reserved for the multi-GPU exchange                          */
+    MARS_ERR_NCCL = 4,       /* NCCL missing or a collective of the multi-GPU exchange failed */
     MARS_ERR_ALL_FAILED = 5  /* "batch failed: no run completed" (runner.cpp:153-155)        */
 };
 
@@ -167,6 +167,30 @@ int mars_run_batch(mars_problem_t* p, const mars_params_t* prm, int64_t runs,
  * each rank runs its shard, the records are gathered, then mars_aggregate). */
 int mars_run_shard(mars_problem_t* p, const mars_params_t* prm, int64_t runs,
                    uint64_t base_seed, int64_t first, int64_t count, mars_records_t* records);
+
+/* ---- multi-GPU inside one call (SURVEY.md 8(b) device set, 8(e)) ------------------------
+ *
+ * mars_problem_replicate: the same problem (host copy, kernel family) stored on `device`.
+ * mars_run_batch_multi: run_batch over `count` replicas on distinct devices -- the run
+ * indices split into contiguous shards, one host thread + stream per device running its
+ * shard, then one exchange over NCCL (loaded at run time; ncclCommInitAll over the devices):
+ * AllReduce(min) of the shard best energies, AllReduce(min) of the first index attaining the
+ * batch best, Broadcast of that run's spins from its owner, AllGather of every shard's
+ * records; the index-order aggregation then runs once.  Results are identical to mars_run_batch
+ * on one device (every run depends only on its index).  MARS_ERR_NCCL when NCCL is missing
+ * or a collective fails.  count == 1 is mars_run_batch. */
+int mars_problem_replicate(const mars_problem_t* p, int32_t device, mars_problem_t** out);
+int mars_run_batch_multi(mars_problem_t* const* replicas, int32_t count, const mars_params_t* prm,
+                         int64_t runs, uint64_t base_seed, mars_records_t* records, mars_stats_t* stats,
+                         int8_t* best_spins);
+/* TEST-ONLY: the shard / exchange logic of mars_run_batch_multi on host memory (the four
+ * collectives between `ranks` host threads) over caller-given full-batch records (status,
+ * energy, cut, descent_iters, elapsed, spins [total*n]); fills records/stats/best_spins like
+ * the multi-device call.  Lets a machine without GPUs test the multi-GPU path. */
+int mars_debug_exchange(int32_t ranks, int64_t total, int32_t n, const uint8_t* status, const double* energy,
+                        const double* cut, const int64_t* iters, const double* elapsed, const int8_t* spins,
+                        double energy_tolerance, mars_records_t* records, mars_stats_t* stats,
+                        int8_t* best_spins);
 
 /* The reference's aggregation (runner.cpp:126-167) over `count` records in index order.
  * energy_tolerance: 0 for integral problems, 1e-9 otherwise (model.hpp:82). */

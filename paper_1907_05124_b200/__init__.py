@@ -19,7 +19,7 @@ _MARS_NAMES = (
     "mars_grid_count", "mars_grid_temp", "mars_run_count", "mars_run_plan", "mars_sweep",
     "round_spins", "run_batch", "run_batch_with", "run_shard", "shard_range",
     "splitmix64", "sub_seed", "time_to_best", "validate", "debug_sweep",
-    "NmfaParams", "SimCimParams", "nmfa_defaults", "simcim_defaults", "linear_schedule", "schedule_at",
+    "NmfaParams", "SimCimParams", "run_batch_multi", "debug_exchange", "nmfa_defaults", "simcim_defaults", "linear_schedule", "schedule_at",
 )
 
 __all__ = list(_MARS_NAMES) + ["io", "mars", "workloads"]

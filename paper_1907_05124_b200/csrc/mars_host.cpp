@@ -23,6 +23,7 @@
 
 #include "../../include/mars_b200.h"
 #include "kernels.cuh"
+#include "host_internal.hpp"
 #include "rng.hpp"
 #include "tma_host.hpp"
 
@@ -877,6 +878,31 @@ int batch_alloc(mars_batch* b) {
 
 }  // namespace
 
+namespace marsb200 {
+
+int host_fail(int code, const std::string& msg) { return fail(code, msg); }
+
+int batch_device_view(mars_batch_t* b, BatchDevView* v) {
+    if (!b || !v) return fail(MARS_ERR_INPUT, "null argument");
+    if (!b->executed) return fail(MARS_ERR_RUNTIME, "batch viewed before execute");
+    *v = BatchDevView{b->p->device, b->p->stream, b->p->n, b->first, b->count, b->d_status, b->d_energy,
+                      b->d_cut, b->d_iters, b->d_elapsed, b->d_spins, b->d_best};
+    return MARS_OK;
+}
+
+int plan_start_temps(const mars_params_t* prm, std::uint64_t base_seed, std::int64_t total, double* out) {
+    parallel_for(total, [&](std::int64_t lo, std::int64_t hi) {
+        for (std::int64_t k = lo; k < hi; ++k) {
+            bool sk;
+            std::uint64_t seed;
+            plan_of(prm, base_seed, k, &sk, &out[k], &seed);
+        }
+    });
+    return MARS_OK;
+}
+
+}  // namespace marsb200
+
 // ============================================================================ C-ABI
 
 extern "C" {
@@ -1072,6 +1098,21 @@ int mars_problem_from_edges(int32_t n, int64_t m, const int32_t* u, const int32_
     mars_problem* p = nullptr;
     if (int rc = host_edges(n, m, u, v, w, h, &p)) return rc;
     return finish_problem(p, device, kernel, out);
+}
+
+// A copy of the problem on another device (same host data, same kernel family): the replicas
+// mars_run_batch_multi shards a batch over.
+int mars_problem_replicate(const mars_problem_t* src, int32_t device, mars_problem_t** out) {
+    if (!src || !out) return fail(MARS_ERR_INPUT, "null argument");
+    auto* p = new mars_problem;
+    p->n = src->n;
+    p->dense = src->dense;
+    p->J = src->J;
+    p->off = src->off;
+    p->idx = src->idx;
+    p->wt = src->wt;
+    p->h = src->h;
+    return finish_problem(p, device, src->kernel, out);
 }
 
 int mars_problem_hash(const mars_problem_t* p, uint64_t* out) {

@@ -311,6 +311,13 @@ class IsingProblem:
                                            _KERNELS[kernel], C.byref(out)))
         return IsingProblem(out.value, n)
 
+    def replicate(self, device: int) -> "IsingProblem":
+        """The same problem stored on another device (mars_problem_replicate): the replicas
+        run_batch_multi shards a batch over."""
+        out = C.c_void_p()
+        _check(lib.mars_problem_replicate(self._h, int(device), C.byref(out)))
+        return IsingProblem(out.value, self.size())
+
     def size(self) -> int:
         return self._n
 
@@ -618,6 +625,42 @@ def run_batch(problem: IsingProblem, spec: BatchSpec, progress: Optional[Progres
     if progress is not None:
         _replay_progress(stats, progress)
     return stats
+
+
+def run_batch_multi(problems: list, spec: BatchSpec) -> BatchStats:
+    """run_batch over several GPUs in ONE native call (mars_run_batch_multi): ``problems`` are
+    replicas of one problem on distinct devices (IsingProblem.replicate); contiguous shards of
+    the run indices run concurrently, one host thread per device, and the records / best spins
+    are exchanged over NCCL (AllReduce-min of the best energy and index, Broadcast of the
+    winning spins, AllGather of the records).  Identical results to run_batch on one device."""
+    validate(spec.params)
+    runs = mars_run_count(spec.params, spec.runs)
+    n = problems[0].size()
+    rec = Records.empty(runs, n, spec.keep_spins)
+    c = rec.c()
+    st = N.mars_stats_t()
+    best = np.zeros(n, np.int8)
+    handles = (C.c_void_p * len(problems))(*[p._h.value for p in problems])
+    _check(lib.mars_run_batch_multi(handles, len(problems), C.byref(spec.params._c()), int(spec.runs),
+                                    int(spec.base_seed), C.byref(c), C.byref(st), ptr(best)))
+    stats = aggregate(rec, problems[0].energy_equality_tolerance(), st.total_seconds)
+    stats.best_result.spins = best
+    return stats
+
+
+def debug_exchange(ranks: int, records: Records, tolerance: float):
+    """TEST-ONLY: mars_run_batch_multi's shard / exchange logic on host memory (host threads as
+    ranks) over given full-batch records; returns (merged Records, BatchStats, best spins)."""
+    total, n = records.spins.shape
+    out = Records.empty(total, n, False)
+    c = out.c()
+    st = N.mars_stats_t()
+    best = np.zeros(n, np.int8)
+    it = np.ascontiguousarray(records.descent_iters, np.int64)
+    _check(lib.mars_debug_exchange(int(ranks), total, n, ptr(records.status), ptr(records.energy),
+                                   ptr(records.cut), ptr(it), ptr(records.elapsed_seconds),
+                                   ptr(records.spins), float(tolerance), C.byref(c), C.byref(st), ptr(best)))
+    return out, st, best
 
 
 def _replay_progress(stats: "BatchStats", progress: ProgressFn) -> None:

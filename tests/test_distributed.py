@@ -76,3 +76,21 @@ def test_gloo_world2_matches_single_process(runs):
         assert got[8] == full.spins[ref.best_index].tolist()   # winner broadcast from its owner
         assert got[9] == full.energy.tolist()            # gathered in run-index order
         assert got[10] == full.spins.tolist()
+
+
+@pytest.mark.parametrize("ranks", [1, 2, 3, 8])
+def test_native_multi_gpu_exchange_logic(ranks):
+    """mars_run_batch_multi's C++ shard / exchange (AllReduce-min of the best energy and of the
+    first index reaching it, Broadcast of the winning spins, AllGather of the records) run on a
+    host transport -- one host thread per rank, the same code the NCCL transport drives --
+    must reproduce the single-shard, index-order aggregation (runner.cpp:126-167) exactly."""
+    runs = 203
+    full = synthetic_records(0, runs, runs)
+    merged, st, best = mb.debug_exchange(ranks, full, 0.0)
+    for name in ("status", "energy", "cut", "descent_iters", "elapsed_seconds"):
+        assert np.array_equal(getattr(merged, name), getattr(full, name)), name
+    ref = mb.aggregate(full, 0.0, 0.0)
+    assert st.best_index == ref.best_index
+    assert st.best_energy == ref.best_energy and st.hit_count == ref.hit_count
+    assert st.mean_energy == ref.mean_energy and st.completed_runs == ref.completed_runs
+    assert np.array_equal(best, full.spins[ref.best_index])
