@@ -58,6 +58,8 @@ typedef struct {
     int64_t nonzeros;
     int32_t device;
     int32_t kernel;          /* MARS_KERNEL_* actually used by mars_run_* on this handle  */
+    int32_t levels;          /* Gauss-Seidel levels of one sweep (sparse layouts; 0 dense) */
+    int32_t reserved;
 } mars_problem_info_t;
 
 /* RunResult fields (solvers.hpp:97-106), one entry per run index, caller-allocated.
@@ -70,6 +72,8 @@ typedef struct {
     int64_t* descent_iters;
     double* elapsed_seconds;
     int8_t* spins;
+    double* fail_temp;       /* Diverged runs: the level temperature T of DivergedError's
+                                "relaxation exceeded the sweep cap at T = " (solvers.cpp:169) */
 } mars_records_t;
 
 /* BatchStats scalars (runner.hpp:29-44); best_index is the run index of best_result. */
@@ -116,8 +120,8 @@ int mars_problem_from_edges(int32_t n, int64_t m, const int32_t* u, const int32_
                             const double* w, const double* h, int32_t device, int32_t kernel,
                             mars_problem_t** out);
 
-/* Staged batches (mars_batch_*) keep their problem alive: with batches outstanding the
- * handle is only marked released and is freed by the last mars_batch_destroy. */
+/* Staged batches (mars_batch_*) keep their problem alive: the handle and every live batch
+ * hold one reference; the last of mars_problem_destroy / mars_batch_destroy frees it. */
 void mars_problem_destroy(mars_problem_t* p);
 int mars_problem_info(const mars_problem_t* p, mars_problem_info_t* out);
 

@@ -31,13 +31,14 @@ class mars_params_t(C.Structure):
 class mars_problem_info_t(C.Structure):
     _fields_ = [("n", C.c_int32), ("uses_adjacency", C.c_int32), ("integral", C.c_int32),
                 ("has_field", C.c_int32), ("coupling_sum", C.c_double), ("nonzeros", C.c_int64),
-                ("device", C.c_int32), ("kernel", C.c_int32)]
+                ("device", C.c_int32), ("kernel", C.c_int32), ("levels", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class mars_records_t(C.Structure):
     _fields_ = [("status", C.c_void_p), ("energy", C.c_void_p), ("cut", C.c_void_p),
                 ("start_temp", C.c_void_p), ("descent_iters", C.c_void_p),
-                ("elapsed_seconds", C.c_void_p), ("spins", C.c_void_p)]
+                ("elapsed_seconds", C.c_void_p), ("spins", C.c_void_p), ("fail_temp", C.c_void_p)]
 
 
 class mars_stats_t(C.Structure):

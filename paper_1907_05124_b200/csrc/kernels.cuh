@@ -38,6 +38,7 @@ struct RelaxArgs {
     long long* iters;
     double* elapsed;
     unsigned long long* done_ns;  // [count] %globaltimer when the run retired, or nullptr
+    double* fail_temp;         // [count] level temperature of a Diverged run, or nullptr
     std::int8_t* spins;        // [count][n] rounded final state (round_spins, model.cpp:245)
     // optional per-CTA phase counters (clock64 cycles), kProfSlots per CTA, or nullptr
     long long* prof;

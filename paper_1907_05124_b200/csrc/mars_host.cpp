@@ -7,6 +7,7 @@
 //   run_batch / run_batch_with          runner.cpp:81-178 (aggregation 126-167)
 // The per-run work itself (descents, energies, best-of-R) runs in the sm_100a kernels.
 #include <atomic>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -106,10 +107,11 @@ void plan_of(const mars_params_t* prm, std::uint64_t base, std::int64_t idx, boo
 // ============================================================================ problem store
 
 struct mars_problem {
-    // staged batches borrow this problem's stream and buffer pool: mars_problem_destroy
-    // with batches alive only marks the handle released, the last mars_batch_destroy frees it
-    std::atomic<int> live_batches{0};
-    std::atomic<bool> released{false};
+    // staged batches borrow this problem's stream and buffer pool: one reference for the handle
+    // and one per live batch; whichever of mars_problem_destroy / mars_batch_destroy drops the
+    // last reference frees the problem (a single atomic count: no double delete)
+    std::atomic<int> refs{1};
+    std::mutex pool_mu;             // the buffer pool is shared by concurrent batches
     int n = 0;
     bool dense = true;              // storage choice of the reference (model.cpp:91)
     bool integral = true;
@@ -165,12 +167,27 @@ struct mars_problem {
     std::vector<PoolBuf> pool;
 
     void* take(std::size_t bytes, bool pinned) {
+        std::lock_guard<std::mutex> lk(pool_mu);
         bytes = std::max<std::size_t>(bytes, 16);
         for (std::size_t k = 0; k < pool.size(); ++k)
             if (pool[k].pinned == pinned && pool[k].bytes >= bytes && pool[k].bytes <= 2 * bytes + 4096) {
                 void* ptr = pool[k].ptr;
                 pool.erase(pool.begin() + static_cast<std::ptrdiff_t>(k));
                 return ptr;
+            }
+        // no pooled block fits: release the idle blocks of this kind first, so a problem that
+        // runs batches of changing sizes keeps one batch's worth of memory, not every size seen
+        for (std::size_t k = pool.size(); k-- > 0;)
+            if (pool[k].pinned == pinned) {
+                void* q = pool[k].ptr;
+                if (pinned) cudaFreeHost(q);
+                else cudaFree(q);
+                for (std::size_t z = 0; z < sizes.size(); ++z)
+                    if (sizes[z].first == q) {
+                        sizes.erase(sizes.begin() + static_cast<std::ptrdiff_t>(z));
+                        break;
+                    }
+                pool.erase(pool.begin() + static_cast<std::ptrdiff_t>(k));
             }
         void* ptr = nullptr;
         if ((pinned ? cudaMallocHost(&ptr, bytes) : cudaMalloc(&ptr, bytes)) != cudaSuccess) return nullptr;
@@ -179,6 +196,7 @@ struct mars_problem {
     }
     void give(void* ptr, bool pinned) {
         if (!ptr) return;
+        std::lock_guard<std::mutex> lk(pool_mu);
         for (const auto& sz : sizes)
             if (sz.first == ptr) {
                 pool.push_back({ptr, sz.second, pinned});
@@ -583,6 +601,7 @@ struct mars_batch {
     long long* d_iters = nullptr;
     double* d_elapsed = nullptr;
     unsigned long long* d_done = nullptr;  // [count] retirement %globaltimer (time-to-best)
+    double* d_failT = nullptr;             // [count] level temperature of a Diverged run
     std::int8_t* d_spins = nullptr;
     double* d_energy = nullptr;
     double* d_cut = nullptr;
@@ -609,7 +628,7 @@ struct mars_batch {
             p->give(h, true);
         for (void* d : {d_s0, static_cast<void*>(d_temp), static_cast<void*>(d_order), d_work,
                         static_cast<void*>(d_queue), static_cast<void*>(d_status), static_cast<void*>(d_iters),
-                        static_cast<void*>(d_elapsed), static_cast<void*>(d_done), static_cast<void*>(d_spins), static_cast<void*>(d_energy),
+                        static_cast<void*>(d_elapsed), static_cast<void*>(d_done), static_cast<void*>(d_failT), static_cast<void*>(d_spins), static_cast<void*>(d_energy),
                         static_cast<void*>(d_cut), static_cast<void*>(d_part_e), static_cast<void*>(d_part_i),
                         static_cast<void*>(d_best)})
             p->give(d, false);
@@ -736,6 +755,8 @@ int batch_alloc(mars_batch* b) {
     if (!(b->d_iters = static_cast<decltype(b->d_iters)>(p->take(cnt * sizeof(long long), false))))
         return fail(MARS_ERR_CUDA, "device allocation failed");
     if (!(b->d_elapsed = static_cast<decltype(b->d_elapsed)>(p->take(cnt * sizeof(double), false))))
+        return fail(MARS_ERR_CUDA, "device allocation failed");
+    if (!(b->d_failT = static_cast<decltype(b->d_failT)>(p->take(cnt * sizeof(double), false))))
         return fail(MARS_ERR_CUDA, "device allocation failed");
     if (!(b->d_done = static_cast<decltype(b->d_done)>(p->take(cnt * sizeof(unsigned long long), false))))
         return fail(MARS_ERR_CUDA, "device allocation failed");
@@ -1146,8 +1167,7 @@ int mars_problem_rows(const mars_problem_t* p, double* out) {
 
 void mars_problem_destroy(mars_problem_t* p) {
     if (!p) return;
-    p->released = true;
-    if (p->live_batches.load() == 0) delete p;
+    if (--p->refs == 0) delete p;
 }
 
 int mars_problem_info(const mars_problem_t* p, mars_problem_info_t* out) {
@@ -1160,6 +1180,8 @@ int mars_problem_info(const mars_problem_t* p, mars_problem_info_t* out) {
     out->nonzeros = p->nnz;
     out->device = p->device;
     out->kernel = p->kernel;
+    out->levels = p->kernel == MARS_KERNEL_CSR ? (p->stencil ? p->st_nlev : p->nlev) : 0;
+    out->reserved = 0;
     return MARS_OK;
 }
 
@@ -1201,7 +1223,7 @@ int mars_batch_create(mars_problem_t* p, const mars_params_t* prm, int64_t runs,
                                         std::to_string(total) + " runs");
     auto* b = new mars_batch;
     b->p = p;
-    ++p->live_batches;
+    ++p->refs;
     b->prm = *prm;
     if (b->prm.sweep_cap == 0) b->prm.sweep_cap = kSweepCap;
     b->runs = total;
@@ -1287,6 +1309,7 @@ int execute_impl(mars_batch_t* b, mars_timing_t* timing, int fixed_sweeps, float
     ra.spins = b->d_spins;
     ra.fixed_sweeps = fixed_sweeps;
     ra.jscale = static_cast<float>(std::ldexp(1.0, -p->jexp));
+    ra.fail_temp = b->d_failT;
     ra.state_out = d_state_out;
     std::int64_t launches = 0;
     const bool prof = std::getenv("MARS_PROFILE") != nullptr;
@@ -1445,6 +1468,7 @@ int mars_batch_fetch(mars_batch_t* b, mars_records_t* rec, int64_t* best_index,
         if (rec->cut && cnt) CUDA_TRY(cudaMemcpyAsync(rec->cut, b->d_cut, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
         if (rec->elapsed_seconds && cnt) CUDA_TRY(cudaMemcpyAsync(rec->elapsed_seconds, b->d_elapsed, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
         if (rec->spins && cnt) CUDA_TRY(cudaMemcpyAsync(rec->spins, b->d_spins, cnt * p->n, cudaMemcpyDeviceToHost, st));
+        if (rec->fail_temp && cnt) CUDA_TRY(cudaMemcpyAsync(rec->fail_temp, b->d_failT, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
     }
     long long best = -1;
     CUDA_TRY(cudaMemcpyAsync(&best, b->d_best, sizeof best, cudaMemcpyDeviceToHost, st));
@@ -1507,7 +1531,7 @@ void mars_batch_destroy(mars_batch_t* b) {
     if (!b) return;
     mars_problem* p = b->p;
     delete b;
-    if (p && --p->live_batches == 0 && p->released) delete p;
+    if (p && --p->refs == 0) delete p;
 }
 
 // runner.cpp:126-167 -- index-order aggregation; the all-failed batch is an error (153-155)
@@ -1574,7 +1598,7 @@ int mars_run_batch(mars_problem_t* p, const mars_params_t* prm, int64_t runs, ui
     std::vector<std::uint8_t> status(total);
     std::vector<double> energy(total), cut(total), elapsed(total);
     mars_records_t own{status.data(), energy.data(), cut.data(), nullptr, nullptr, elapsed.data(),
-                       records ? records->spins : nullptr};
+                       records ? records->spins : nullptr, records ? records->fail_temp : nullptr};
     if (records) {
         own.start_temp = records->start_temp;
         own.descent_iters = records->descent_iters;

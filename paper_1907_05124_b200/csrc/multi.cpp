@@ -472,6 +472,12 @@ int mars_run_batch_multi(mars_problem_t* const* replicas, int32_t count, const m
                                       static_cast<std::size_t>(v.count) * n, cudaMemcpyDeviceToHost) != cudaSuccess)
                 return host_fail(MARS_ERR_CUDA, "spins D2H failed");
         }
+    if (records && records->fail_temp)
+        for (int r = 0; r < count; ++r) {
+            mars_records_t part{};
+            part.fail_temp = records->fail_temp + views[r].first;
+            if (int e = mars_batch_fetch(batches[r], &part, nullptr, nullptr)) return e;
+        }
     if (records && records->start_temp) plan_start_temps(prm, base_seed, total, records->start_temp);
     const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return finish(m, total, info[0].integral ? 0.0 : 1e-9, secs, records, stats, best_spins, n);

@@ -342,6 +342,10 @@ class IsingProblem:
     def kernel(self) -> str:
         return _KERNEL_NAMES[int(self._info.kernel)]
 
+    def levels(self) -> int:
+        """Gauss-Seidel levels of one sweep in the sparse layouts (0 for dense kernels)."""
+        return int(self._info.levels)
+
     def energy_equality_tolerance(self) -> float:
         """model.hpp:82."""
         return 0.0 if self.integral() else 1e-9
@@ -414,25 +418,33 @@ class Records:
     descent_iters: np.ndarray
     elapsed_seconds: np.ndarray
     spins: Optional[np.ndarray] = None   # [runs, n] int8 when requested
+    fail_temp: Optional[np.ndarray] = None  # level temperature of Diverged runs (their message)
 
     @staticmethod
     def empty(count: int, n: int, with_spins: bool) -> "Records":
         return Records(np.zeros(count, np.uint8), np.zeros(count), np.zeros(count),
                        np.zeros(count), np.zeros(count, np.int64), np.zeros(count),
-                       np.zeros((count, n), np.int8) if with_spins else None)
+                       np.zeros((count, n), np.int8) if with_spins else None, np.zeros(count))
 
     def c(self) -> N.mars_records_t:
         return N.mars_records_t(ptr(self.status), ptr(self.energy), ptr(self.cut),
                                 ptr(self.start_temp), ptr(self.descent_iters),
-                                ptr(self.elapsed_seconds), ptr(self.spins))
+                                ptr(self.elapsed_seconds), ptr(self.spins), ptr(self.fail_temp))
+
+    def error(self, k: int) -> str:
+        """RunResult::error of a Diverged run: DivergedError's message (solvers.cpp:169,
+        std::to_string(t) == printf("%f", t))."""
+        if self.status[k] != RunStatus.Diverged:
+            return ""
+        t = float(self.fail_temp[k]) if self.fail_temp is not None else 0.0
+        return "relaxation exceeded the sweep cap at T = " + ("%f" % t)
 
     def result(self, k: int) -> RunResult:
         st = RunStatus(int(self.status[k]))
         return RunResult(st, float(self.energy[k]), float(self.cut[k]),
                          None if self.spins is None or st == RunStatus.Skipped else self.spins[k].copy(),
                          float(self.start_temp[k]), int(self.descent_iters[k]),
-                         float(self.elapsed_seconds[k]),
-                         "relaxation exceeded the sweep cap" if st == RunStatus.Diverged else "")
+                         float(self.elapsed_seconds[k]), self.error(k))
 
 
 @dataclass
@@ -529,7 +541,7 @@ def gather_records(dist, local: Records, runs: int, n: int, keep_spins: bool) ->
     backend = dist.get_backend()
     dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
     out = Records.empty(runs, n, keep_spins)
-    fields = ["status", "energy", "cut", "start_temp", "descent_iters", "elapsed_seconds"]
+    fields = ["status", "energy", "cut", "start_temp", "descent_iters", "elapsed_seconds", "fail_temp"]
     cap = max(shard_range(runs, r, world)[1] for r in range(world))
     for name in fields:
         arr = getattr(local, name)

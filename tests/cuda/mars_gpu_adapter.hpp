@@ -69,11 +69,11 @@ inline BatchStats run_batch(const DeviceProblem& dp, const BatchSpec& spec,
     check(mars_run_count(&prm, spec.runs, &runs));
     const int n = dp.size();
     std::vector<uint8_t> status(runs);
-    std::vector<double> energy(runs), cut(runs), temp(runs), elapsed(runs);
+    std::vector<double> energy(runs), cut(runs), temp(runs), elapsed(runs), fail_temp(runs);
     std::vector<int64_t> iters(runs);
     std::vector<int8_t> spins(static_cast<size_t>(runs) * n);
     mars_records_t rec{status.data(), energy.data(), cut.data(), temp.data(), iters.data(),
-                       elapsed.data(), spins.data()};
+                       elapsed.data(), spins.data(), fail_temp.data()};
     mars_stats_t st{};
     check(mars_run_batch(dp.handle(), &prm, spec.runs, spec.base_seed, &rec, &st, nullptr));
 
@@ -90,7 +90,8 @@ inline BatchStats run_batch(const DeviceProblem& dp, const BatchSpec& spec,
         r.elapsed_seconds = elapsed[k];
         if (r.status != RunStatus::Skipped)
             r.spins.assign(spins.begin() + k * n, spins.begin() + (k + 1) * n);
-        if (r.status == RunStatus::Diverged) r.error = "relaxation exceeded the sweep cap";
+        if (r.status == RunStatus::Diverged)
+            r.error = "relaxation exceeded the sweep cap at T = " + std::to_string(fail_temp[k]);
         if (r.status == RunStatus::Ok) {
             out.energies.push_back(r.energy);
             best_so_far = std::min(best_so_far, r.energy);

@@ -195,6 +195,17 @@ def test_divergence_records_match_port(port):
     both_div = (stats.records.status == 2) & (ob.status == 2)
     assert np.all(stats.records.descent_iters[both_div] <= 40)
     assert stats.completed_runs == (stats.records.status == 0).sum()
+    # a Diverged record is built fresh (runner.cpp:43-53): elapsed 0, DivergedError's message with
+    # the level temperature formatted by std::to_string (solvers.cpp:169)
+    div = np.flatnonzero(stats.records.status == 2)
+    assert np.all(stats.records.elapsed_seconds[div] == 0.0)
+    for k in div[:8]:
+        msg = stats.runs[k].error
+        assert msg.startswith("relaxation exceeded the sweep cap at T = ")
+        t = float(msg.rsplit("= ", 1)[1])
+        assert msg.endswith("%f" % t)
+        levels = stats.records.start_temp[k] - np.arange(1, 64)
+        assert np.min(np.abs(levels - t)) < 1e-5
 
 
 def test_all_failed_batch_raises():
