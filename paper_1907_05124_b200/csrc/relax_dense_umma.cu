@@ -161,8 +161,27 @@ __device__ __forceinline__ int tri_row_off_rt(int i) {
 // in a register (del[I]) -- the walker stores the sub-block's Deltas to TMEM for the helper.
 constexpr int SB = 16;
 
+// The same for row i = k0 + I with k0 a multiple of 16 and I < 16 a compile-time constant:
+// with Q = k0 / 4, a = I / 4, r = I % 4 the closed form of tri_row_off(i) - tri_k0(i) is
+//   (128 k0 - 8 Q^2 - k0) + (128 I - 8 a^2 - 4 a (r - 1) - ((I + 1) & ~3)) - Q (4 (r - 1) + 16 a),
+// i.e. a per-sub-block base plus a constant minus Q times a constant: one IMAD per row.
+struct TriRows {
+    const float* base;    // jtri + 128 k0 - 8 Q^2 - k0
+    int Q;
+    __device__ __forceinline__ TriRows(const float* jtri, int k0) : base(jtri + 127 * k0 - 8 * (k0 >> 2) * (k0 >> 2)), Q(k0 >> 2) {}
+    template <int I>
+    __device__ __forceinline__ const float* row(int col) const {   // &J[k0 + I][col]
+        constexpr int a = I >> 2, r = I & 3;
+        constexpr int kc = 128 * I - 8 * a * a - 4 * a * (r - 1) - ((I + 1) & ~3);
+        constexpr int kq = 4 * (r - 1) + 16 * a;
+        return base + kc - Q * kq + col;
+    }
+};
+static_assert(TB == 128, "TriRows assumes 128-spin blocks");
+
 struct SubCtx {
     const float* jtri;
+    TriRows tr;           // rows of the current sub-block
     const float* h;       // field slice or nullptr
     float T;              // level temperature (fp32)
     float rT;             // recip_for_div(T), or 0 at the quench
@@ -175,10 +194,12 @@ __device__ __forceinline__ float2 ffma2(float2 a, float b, float2 c) {
     return __ffma2_rn(a, make_float2(b, b), c);
 }
 
-// address of J[i][k0 + m], m >= tri_k0(i) - k0, inside the packed triangle
+// address of J[i][col], col >= tri_k0(i), inside the packed triangle
 __device__ __forceinline__ const float* tri_ptr(const float* jtri, int i, int col) {
     return jtri + tri_row_off_rt(i) - tri_k0(i) + col;
 }
+
+
 
 template <int I, int G>
 __device__ __forceinline__ void sub_update_group(float2 (&p)[SB / 2], const float4 j, float d) {
@@ -209,7 +230,7 @@ __device__ __forceinline__ void sub_step(float2 (&p)[SB / 2], float2 (&an)[SB / 
         // J[k0+I][k0 + 4g ..] for the groups this spin updates, issued before the trial
         float4 jr[SB / 4];
         if constexpr (I + 1 < SB) {
-            const float* row = tri_ptr(c.jtri, k0 + I, k0);   // row[m] = J[k0+I][k0+m]
+            const float* row = c.tr.template row<I>(k0);     // row[m] = J[k0+I][k0+m]
 #pragma unroll
             for (int g = ((I + 1) & ~3) / 4; g < SB / 4; ++g) jr[g] = *reinterpret_cast<const float4*>(row + 4 * g);
         }
@@ -229,7 +250,7 @@ __device__ __forceinline__ void sub_step(float2 (&p)[SB / 2], float2 (&an)[SB / 
             sub_update<I>(p, jr, delta, std::make_integer_sequence<int, SB / 4 - ((I + 1) & ~3) / 4>{});
         // this spin's coupling to the NEXT sub-block's fields, accumulated off the serial chain
         // (fills the walk's idle issue slots; added to the next sub-block's fields before it walks)
-        const float4* jn = reinterpret_cast<const float4*>(tri_ptr(c.jtri, k0 + I, k0 + SB));
+        const float4* jn = reinterpret_cast<const float4*>(c.tr.template row<I>(k0 + SB));
 #pragma unroll
         for (int g = 0; g < SB / 4; ++g) {
             const float4 jv = jn[g];
@@ -260,18 +281,28 @@ __device__ __forceinline__ void walk_dispatch(float2 (&p)[SB / 2], float2 (&an)[
 
 // fields (fp32 pairs) += J[j0 .. j0+16)[col .. col+16)^T * d[0..16): the 16 x 16 rectangle
 // coupling one sub-block's Deltas to a later sub-block's fields (rows from the triangle)
+template <int J>
+__device__ __forceinline__ void rect_row(float2 (&pf)[SB / 2], const TriRows& tr, int col, float d) {
+    const float4* jr = reinterpret_cast<const float4*>(tr.template row<J>(col));
+#pragma unroll
+    for (int m = 0; m < SB / 4; ++m) {
+        const float4 jv = jr[m];
+        pf[2 * m] = ffma2(make_float2(jv.x, jv.y), d, pf[2 * m]);
+        pf[2 * m + 1] = ffma2(make_float2(jv.z, jv.w), d, pf[2 * m + 1]);
+    }
+}
+
+template <int... J>
+__device__ __forceinline__ void rect_rows(float2 (&pf)[SB / 2], const TriRows& tr, int col, const float (&d)[SB],
+                                          std::integer_sequence<int, J...>) {
+    (rect_row<J>(pf, tr, col, d[J]), ...);
+}
+
+// fields (fp32 pairs) += J[j0 .. j0+16)[col .. col+16)^T * d[0..16): the 16 x 16 rectangle
+// coupling one sub-block's Deltas to a later sub-block's fields (rows from the triangle)
 __device__ __forceinline__ void apply_rect16(float2 (&pf)[SB / 2], const float* jtri, int j0, int col,
                                              const float (&d)[SB]) {
-#pragma unroll
-    for (int j = 0; j < SB; ++j) {
-        const float4* jr = reinterpret_cast<const float4*>(tri_ptr(jtri, j0 + j, col));
-#pragma unroll
-        for (int m = 0; m < SB / 4; ++m) {
-            const float4 jv = jr[m];
-            pf[2 * m] = ffma2(make_float2(jv.x, jv.y), d[j], pf[2 * m]);
-            pf[2 * m + 1] = ffma2(make_float2(jv.z, jv.w), d[j], pf[2 * m + 1]);
-        }
-    }
+    rect_rows(pf, TriRows(jtri, j0), col, d, std::make_integer_sequence<int, SB>{});
 }
 
 __device__ __forceinline__ void tmem_ld16(std::uint32_t taddr, float (&v)[16]) {
@@ -624,7 +655,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 t0 = clock64();
                 c_wait += t0 - t1;
                 const std::uint32_t tacc = tmem + lane_t + buf * TB;
-                SubCtx ctx{jtri, a.h32 ? a.h32 + b0 : nullptr, Tf, rT, quench, lim, 0.0f};
+                SubCtx ctx{jtri, TriRows(jtri, 0), a.h32 ? a.h32 + b0 : nullptr, Tf, rT, quench, lim, 0.0f};
                 float prev[SB];                                 // this sub-block's Deltas
                 float2 an[SB / 2];                              // previous sub-block's coupling
 #pragma unroll                                                  // to this one (built during its walk)
@@ -654,6 +685,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     c_f += t0 - t1;
                     t1 = t0;
                     float nv[SB];
+                    ctx.tr = TriRows(jtri, k0);
                     if (ctx.h) walk_dispatch<true>(pf, an, old, nv, prev, k0, ctx);
                     else walk_dispatch<false>(pf, an, old, nv, prev, k0, ctx);
                     t0 = clock64();

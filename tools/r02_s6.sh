@@ -12,5 +12,5 @@ print(k, float(np.abs(out).mean()))
 PY
 timeout 300 python /tmp/exp6.py > gpurun_out/s6/plain.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:relax_dense_umma -c 1 \
-  -o gpurun_out/s6/umma_full python /tmp/exp6.py > gpurun_out/s6/ncu.log 2>&1
+  -o gpurun_out/s6/umma_pair_full python /tmp/exp6.py > gpurun_out/s6/ncu.log 2>&1
 echo done
