@@ -167,6 +167,17 @@ int mars_run_batch(mars_problem_t* p, const mars_params_t* prm, int64_t runs,
                    uint64_t base_seed, mars_records_t* records, mars_stats_t* stats,
                    int8_t* best_spins);
 
+/* run_batch with a ProgressFn (runner.hpp:52-56): progress(run index, best energy so far,
+ * user) is called from the calling thread once per run while the batch runs -- in completion
+ * order, best_so_far non-increasing, skipped grid slots first -- as the reference's worker
+ * pool does (runner.cpp:107-113).  The kernels log each run into host-mapped memory when its
+ * rounded spins are written; the finished runs' exact energies are evaluated on a side stream
+ * (concurrently with the relaxation kernel when it leaves SMs free, else right after it). */
+int mars_run_batch_progress(mars_problem_t* p, const mars_params_t* prm, int64_t runs,
+                            uint64_t base_seed, mars_records_t* records, mars_stats_t* stats,
+                            int8_t* best_spins, void (*progress)(int64_t index, double best_so_far, void* user),
+                            void* user);
+
 /* A contiguous shard [first, first+count) of the batch's run indices (for multi-GPU:
  * each rank runs its shard, the records are gathered, then mars_aggregate). */
 int mars_run_shard(mars_problem_t* p, const mars_params_t* prm, int64_t runs,

@@ -67,6 +67,7 @@ class mars_simcim_params_t(C.Structure):
 
 
 vp, i32, i64, u64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double
+PROGRESS_FN = C.CFUNCTYPE(None, C.c_int64, C.c_double, C.c_void_p)   # progress(index, best, user)
 P_params = C.POINTER(mars_params_t)
 
 # name -> (restype, argtypes): exactly the declarations of include/mars_b200.h
@@ -97,6 +98,7 @@ SIGNATURES = {
     "mars_batch_execute": (C.c_int, [vp, C.POINTER(mars_timing_t)]),
     "mars_debug_sweeps": (C.c_int, [vp, i64, vp, vp, i32, vp, vp]),
     "mars_debug_rng": (C.c_int, [vp, i32, i32, vp, vp]),
+    "mars_run_batch_progress": (C.c_int, [vp, P_params, i64, u64, vp, vp, vp, vp, vp]),
     "mars_problem_replicate": (C.c_int, [vp, i32, C.POINTER(vp)]),
     "mars_run_batch_multi": (C.c_int, [vp, i32, P_params, i64, u64, vp, vp, vp]),
     "mars_debug_exchange": (C.c_int, [i32, i64, i32, vp, vp, vp, vp, vp, vp, dbl, vp, vp, vp]),

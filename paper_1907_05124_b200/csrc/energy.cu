@@ -49,6 +49,37 @@ __global__ void __launch_bounds__(128) energy_kernel(EnergyArgs a) {
     a.cut[r] = 0.25 * (a.coupling_sum - total);
 }
 
+// progress: the same exact-order energy for a list of finished runs, compact outputs
+__global__ void __launch_bounds__(128) energy_list_kernel(EnergyArgs a, const int* list, double* out_e,
+                                                           std::uint8_t* out_st) {
+    const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= a.count) return;
+    const int r = list[k];
+    const int n = a.n;
+    const std::int8_t* s = a.spins + static_cast<size_t>(r) * n;
+    double total = 0.0;
+    if (a.J64) {
+        for (int i = 0; i < n; ++i) {
+            const double* Jr = a.J64 + static_cast<size_t>(i) * n;
+            double row = 0.0;
+            for (int j = 0; j < n; ++j) row += __ldg(Jr + j) * static_cast<double>(s[j]);
+            total += static_cast<double>(s[i]) * row;
+        }
+    } else {
+        for (int i = 0; i < n; ++i) {
+            double row = 0.0;
+            for (int q = __ldg(a.off + i), e = __ldg(a.off + i + 1); q < e; ++q)
+                row += __ldg(a.w64 + q) * static_cast<double>(s[__ldg(a.idx + q)]);
+            total += static_cast<double>(s[i]) * row;
+        }
+    }
+    double e = total;
+    if (a.h64)
+        for (int i = 0; i < n; ++i) e += __ldg(a.h64 + i) * static_cast<double>(s[i]);
+    out_e[k] = e;
+    out_st[k] = *reinterpret_cast<volatile const std::uint8_t*>(a.status + r);
+}
+
 struct Best {
     double e;
     long long i;
@@ -216,6 +247,13 @@ cudaError_t launch_energy(const EnergyArgs& a, cudaStream_t st) {
     }
     const unsigned grid = static_cast<unsigned>((a.count + 127) / 128);
     energy_kernel<<<grid, 128, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_energy_list(const EnergyArgs& a, const int* list, double* out_e, std::uint8_t* out_st,
+                               cudaStream_t st) {
+    if (a.count <= 0) return cudaSuccess;
+    energy_list_kernel<<<static_cast<unsigned>((a.count + 127) / 128), 128, 0, st>>>(a, list, out_e, out_st);
     return cudaGetLastError();
 }
 

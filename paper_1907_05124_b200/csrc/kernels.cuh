@@ -50,6 +50,10 @@ struct RelaxArgs {
     float* state_out;
     // tcgen05 kernel: the field GEMM runs on J * 2^k (fp16 range); fields scale back by 2^-k
     float jscale;
+    // progress during the batch (mars_run_batch_progress): when a run's rounded spins are in
+    // memory its index is appended here (host-mapped, completion order), or nullptr
+    int* retire_log;
+    int* retire_head;          // device counter of retire_log entries
 };
 constexpr int kProfSlots = 16;
 
@@ -210,6 +214,9 @@ cudaError_t launch_brute_force(const double* J, const double* h, int n, double* 
                                int blocks, cudaStream_t st);
 
 cudaError_t launch_energy(const EnergyArgs& a, cudaStream_t st);
+// energies of the runs list[0..a.count) (thread per run), compact outputs out_e / out_st [a.count]
+cudaError_t launch_energy_list(const EnergyArgs& a, const int* list, double* out_e, std::uint8_t* out_st,
+                               cudaStream_t st);
 cudaError_t launch_best(const BestArgs& a, int grid, cudaStream_t st);
 
 }  // namespace marsb200

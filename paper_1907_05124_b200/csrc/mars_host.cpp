@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -1276,7 +1277,78 @@ namespace {
 
 // The device work of one batch (relax -> energy -> reduce).  fixed_sweeps / d_state_out are
 // the test-only fixed-temperature mode of mars_debug_sweeps (RelaxArgs::fixed_sweeps).
-int execute_impl(mars_batch_t* b, mars_timing_t* timing, int fixed_sweeps, float* d_state_out) {
+// Progress during the batch (mars_run_batch_progress): the relaxation kernels append each run
+// whose rounded spins are written to a host-mapped log (completion order); the calling thread
+// polls it while the kernel runs, evaluates those runs' exact energies on a side stream and
+// calls progress(index, best so far) once per run, like the reference's mutex-serialised
+// worker callback (runner.cpp:107-113).  Skipped grid slots are reported first.
+struct ProgressCtx {
+    void (*cb)(int64_t, double, void*);
+    void* user;
+};
+
+int report_progress(mars_batch_t* b, const ProgressCtx& pc, int* h_log, int* d_list_buf, double* d_e, std::uint8_t* d_st,
+                    int* h_list, double* h_e, std::uint8_t* h_st) {
+    mars_problem* p = b->p;
+    double best = std::numeric_limits<double>::infinity();
+    for (std::int64_t k = 0; k < b->count; ++k)
+        if (b->skipped[k]) pc.cb(b->first + k, best, pc.user);
+    cudaStream_t side = nullptr;
+    CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    struct S {
+        cudaStream_t s;
+        ~S() { cudaStreamDestroy(s); }
+    } sg{side};
+    cudaEvent_t done = nullptr;
+    CUDA_TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    struct E {
+        cudaEvent_t e;
+        ~E() { cudaEventDestroy(e); }
+    } eg{done};
+    const int total = b->queue_len;
+    int seen = 0, reported = 0, job = 0;
+    bool inflight = false;
+    const volatile int* log = h_log;
+    while (reported < total) {
+        if (!inflight && seen < total) {
+            int k = 0;
+            while (seen < total && log[seen] >= 0 && k < total) h_list[k++] = log[seen++];
+            if (k > 0) {
+                job = k;
+                CUDA_TRY(cudaMemcpyAsync(d_list_buf, h_list, k * sizeof(int), cudaMemcpyHostToDevice, side));
+                EnergyArgs ea{p->n, p->dJ64, p->dOff, p->dIdx, p->dW64, p->dH64, p->coupling_sum, k, b->d_spins,
+                              b->d_status, nullptr, nullptr};
+                CUDA_TRY(launch_energy_list(ea, d_list_buf, d_e, d_st, side));
+                CUDA_TRY(cudaMemcpyAsync(h_e, d_e, k * sizeof(double), cudaMemcpyDeviceToHost, side));
+                CUDA_TRY(cudaMemcpyAsync(h_st, d_st, k, cudaMemcpyDeviceToHost, side));
+                CUDA_TRY(cudaEventRecord(done, side));
+                inflight = true;
+            }
+        }
+        if (inflight) {
+            const cudaError_t q = cudaEventQuery(done);
+            if (q == cudaSuccess) {
+                for (int k = 0; k < job; ++k) {
+                    if (h_st[k] == MARS_RUN_OK && h_e[k] < best) best = h_e[k];
+                    pc.cb(b->first + h_list[k], best, pc.user);
+                }
+                reported += job;
+                inflight = false;
+                continue;
+            }
+            if (q != cudaErrorNotReady) return fail(MARS_ERR_CUDA, std::string("progress: ") + cudaGetErrorString(q));
+        }
+        const cudaError_t k = cudaStreamQuery(p->stream);          // a relaxation fault ends the wait
+        if (k != cudaSuccess && k != cudaErrorNotReady) return fail(MARS_ERR_CUDA, cudaGetErrorString(k));
+        if (k == cudaSuccess && !inflight && seen == total && reported < total)
+            return fail(MARS_ERR_RUNTIME, "progress: the relaxation kernel ended with runs unreported");
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    return MARS_OK;
+}
+
+int execute_impl(mars_batch_t* b, mars_timing_t* timing, int fixed_sweeps, float* d_state_out,
+                 const ProgressCtx* prog = nullptr) {
     if (!b) return fail(MARS_ERR_INPUT, "null argument");
     if (!b->uploaded) return fail(MARS_ERR_RUNTIME, "batch executed before upload");
     mars_problem* p = b->p;
@@ -1310,6 +1382,44 @@ int execute_impl(mars_batch_t* b, mars_timing_t* timing, int fixed_sweeps, float
     ra.fixed_sweeps = fixed_sweeps;
     ra.jscale = static_cast<float>(std::ldexp(1.0, -p->jexp));
     ra.fail_temp = b->d_failT;
+    // progress buffers: host-mapped completion log + device counter + side-stream scratch
+    int* h_log = nullptr;
+    int* d_head = nullptr;
+    int* d_list = nullptr;
+    double* d_pe = nullptr;
+    std::uint8_t* d_pst = nullptr;
+    std::vector<int> h_list;
+    std::vector<double> h_pe;
+    std::vector<std::uint8_t> h_pst;
+    struct ProgFree {
+        int** hl;
+        std::vector<void*> d;
+        ~ProgFree() {
+            if (*hl) cudaFreeHost(*hl);
+            for (void* x : d) cudaFree(x);
+        }
+    } pfree{&h_log, {}};
+    if (prog && b->queue_len > 0) {
+        const std::size_t q = static_cast<std::size_t>(b->queue_len);
+        CUDA_TRY(cudaHostAlloc(&h_log, q * sizeof(int), cudaHostAllocMapped));
+        std::fill(h_log, h_log + q, -1);
+        int* d_log = nullptr;
+        CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_log), h_log, 0));
+        CUDA_TRY(cudaMalloc(&d_head, sizeof(int)));
+        pfree.d.push_back(d_head);
+        CUDA_TRY(cudaMalloc(&d_list, q * sizeof(int)));
+        pfree.d.push_back(d_list);
+        CUDA_TRY(cudaMalloc(&d_pe, q * sizeof(double)));
+        pfree.d.push_back(d_pe);
+        CUDA_TRY(cudaMalloc(&d_pst, q));
+        pfree.d.push_back(d_pst);
+        CUDA_TRY(cudaMemsetAsync(d_head, 0, sizeof(int), st));
+        h_list.resize(q);
+        h_pe.resize(q);
+        h_pst.resize(q);
+        ra.retire_log = d_log;
+        ra.retire_head = d_head;
+    }
     ra.state_out = d_state_out;
     std::int64_t launches = 0;
     const bool prof = std::getenv("MARS_PROFILE") != nullptr;
@@ -1334,6 +1444,15 @@ int execute_impl(mars_batch_t* b, mars_timing_t* timing, int fixed_sweeps, float
                          : b->use_spmm ? launch_relax_spmm(ra, sparse_levels(p), b->spmm, st)
                                        : launch_relax_sparse(ra, sparse_levels(p), b->sparse, st));
         ++launches;
+    }
+    if (prog) {
+        if (b->queue_len > 0) {
+            if (int rc = report_progress(b, *prog, h_log, d_list, d_pe, d_pst, h_list.data(), h_pe.data(), h_pst.data()))
+                return rc;
+        } else {
+            for (std::int64_t k = 0; k < b->count; ++k)
+                prog->cb(b->first + k, std::numeric_limits<double>::infinity(), prog->user);
+        }
     }
     CUDA_TRY(cudaEventRecord(b->ev[1], st));
     EnergyArgs ea{p->n, p->dJ64, p->dOff, p->dIdx, p->dW64, p->dH64, p->coupling_sum,
@@ -1589,6 +1708,12 @@ int mars_run_shard(mars_problem_t* p, const mars_params_t* prm, int64_t runs, ui
 
 int mars_run_batch(mars_problem_t* p, const mars_params_t* prm, int64_t runs, uint64_t base_seed,
                    mars_records_t* records, mars_stats_t* stats, int8_t* best_spins) {
+    return mars_run_batch_progress(p, prm, runs, base_seed, records, stats, best_spins, nullptr, nullptr);
+}
+
+int mars_run_batch_progress(mars_problem_t* p, const mars_params_t* prm, int64_t runs, uint64_t base_seed,
+                            mars_records_t* records, mars_stats_t* stats, int8_t* best_spins,
+                            void (*progress)(int64_t, double, void*), void* user) {
     const auto t0 = std::chrono::steady_clock::now();
     if (!p || !stats) return fail(MARS_ERR_INPUT, "null argument");
     std::int64_t total = 0;
@@ -1604,8 +1729,9 @@ int mars_run_batch(mars_problem_t* p, const mars_params_t* prm, int64_t runs, ui
         own.descent_iters = records->descent_iters;
     }
     std::int64_t best = -1;
+    const ProgressCtx pc{progress, user};
     int rc = mars_batch_upload(b);
-    if (!rc) rc = mars_batch_execute(b, nullptr);
+    if (!rc) rc = execute_impl(b, nullptr, 0, nullptr, progress ? &pc : nullptr);
     if (!rc) rc = mars_batch_fetch(b, &own, &best, best_spins);
     mars_batch_destroy(b);
     if (rc) return rc;

@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(512) relax_levels_kernel(RelaxArgs a, SparseLe
             for (int i = tid; i < n; i += blockDim.x) out[i] = st[static_cast<size_t>(i) * RUNS + r] < 0.0 ? -1 : 1;
             __syncthreads();
             if (tid == 0) {
+                log_retired(a, slots[r].run);
                 const int run = claim_run(a);
                 if (run >= 0) slot_start(slots[r], run, a);
                 else slots[r].run = -1;

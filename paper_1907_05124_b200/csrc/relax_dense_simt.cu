@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(NT, 1) relax_dense_simt_kernel(RelaxArgs a) {
         }
         __syncthreads();
         if (tid < TM) {
+            if (sm.retire[tid] >= 0) log_retired(a, sm.retire[tid]);
             sm.retire[tid] = -1;
             sm.refill[tid] = -1;
         }

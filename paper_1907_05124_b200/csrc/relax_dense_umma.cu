@@ -720,10 +720,12 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                             mode = new_run >= 0 ? kLoading : kDrain;
                         }
                     } else if (mode == kLoading) {
+                        if (old_run >= 0) log_retired(a, old_run);   // its spins went out this sweep
                         slot_start(slot, new_run, a);
                         mode = kActive;
                         old_run = -1;
                     } else if (mode == kDrain) {
+                        if (old_run >= 0) log_retired(a, old_run);
                         mode = kIdle;
                         old_run = -1;
                     }

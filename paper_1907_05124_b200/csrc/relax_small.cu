@@ -131,6 +131,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32, 1) relax_small_kernel(RelaxA
                 if (k + 1 < n) so[k + 1] = s[p].y;
             }
         }
+        __syncwarp();
+        if (lane == 0) log_retired(a, run);
     }
 }
 

@@ -268,6 +268,8 @@ relax_spmm_kernel(RelaxArgs a, SparseLevels g, int ring_bytes) {
                     const int done = __shfl_sync(gmask, s == 0 ? slots[my + r].run : 0, h * CWR);
                     std::int8_t* out = a.spins + static_cast<std::size_t>(done) * n;
                     for (int i = s; i < n; i += CWR) out[i] = st[static_cast<std::size_t>(i) * R + r] < 0.0 ? -1 : 1;
+                    __syncwarp(gmask);
+                    if (s == 0) log_retired(a, done);
                     int run = -1;
                     if (s == 0) {
                         run = claim_run(a);

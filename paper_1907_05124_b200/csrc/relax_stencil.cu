@@ -139,6 +139,10 @@ __global__ void __launch_bounds__(1024, 1) relax_stencil_kernel(RelaxArgs a, Ste
         if (tid == 0) slot_finish(slot, code, a);
         std::int8_t* out = a.spins + static_cast<std::size_t>(slot.run) * n;
         for (int i = tid; i < n; i += blockDim.x) out[i] = st[i] < 0.0 ? -1 : 1;
+        if (a.retire_log) {
+            __syncthreads();
+            if (tid == 0) log_retired(a, slot.run);
+        }
     }
 }
 

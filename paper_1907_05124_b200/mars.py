@@ -607,8 +607,10 @@ def run_batch(problem: IsingProblem, spec: BatchSpec, progress: Optional[Progres
     """run_batch (runner.hpp:55-56, runner.cpp:170-178).
 
     Validates first (InputError before any run), runs every index on the GPU(s), and
-    aggregates in run-index order exactly like the reference.  ``progress`` is invoked
-    once per run index, in index order, after the batch (runs complete inside one kernel).
+    aggregates in run-index order exactly like the reference.  ``progress(index, best_so_far)``
+    is invoked once per run while the batch runs, in completion order with a non-increasing
+    best (runner.cpp:107-113; mars_run_batch_progress); under torch.distributed it is replayed
+    in index order after the gather.
     """
     validate(spec.params)
     if isinstance(spec.params, (NmfaParams, SimCimParams)):
@@ -630,10 +632,17 @@ def run_batch(problem: IsingProblem, spec: BatchSpec, progress: Optional[Progres
         c = rec.c()
         st = N.mars_stats_t()
         best = np.zeros(n, np.int8)
-        _check(lib.mars_run_batch(problem._h, C.byref(spec.params._c()), int(spec.runs),
-                                  int(spec.base_seed), C.byref(c), C.byref(st), ptr(best)))
+        if progress is None:
+            _check(lib.mars_run_batch(problem._h, C.byref(spec.params._c()), int(spec.runs),
+                                      int(spec.base_seed), C.byref(c), C.byref(st), ptr(best)))
+        else:
+            # called from this thread while the batch runs (mars_run_batch_progress)
+            cb = N.PROGRESS_FN(lambda idx, best_so_far, _user: progress(int(idx), float(best_so_far)))
+            _check(lib.mars_run_batch_progress(problem._h, C.byref(spec.params._c()), int(spec.runs),
+                                               int(spec.base_seed), C.byref(c), C.byref(st), ptr(best), cb, None))
         stats = aggregate(rec, problem.energy_equality_tolerance(), st.total_seconds)
         stats.best_result.spins = best
+        return stats
     if progress is not None:
         _replay_progress(stats, progress)
     return stats

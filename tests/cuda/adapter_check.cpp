@@ -80,6 +80,61 @@ int main() {
         for (int b = a + 1; b < 300; ++b)
             if (r.uniform_open01() < 0.02) edges.push_back({a, b, r.uniform_open01() < 0.5 ? -1.0 : 1.0});
     compare("er300 (CSR)", IsingProblem::from_edges(300, edges), uni, 256, 5, 0.98);
+    // ProgressFn (runner.hpp:52; test_runner.cpp:148-162): once per run incl. the skipped slot,
+    // non-increasing best, on the calling thread while the GPU batch runs
+    {
+        MarsParams g2;
+        g2.t_min = 0;
+        g2.t_max = 10;
+        g2.t_step = 1;
+        BatchSpec spec;
+        spec.params = g2;
+        spec.base_seed = 2;
+        int calls = 0;
+        bool monotone = true;
+        double last = 1e300;
+        const BatchStats gpu = gpu::run_batch(sk(10, 75), spec, [&](std::int64_t, double best) {
+            ++calls;
+            if (best > last + 1e-12) monotone = false;
+            last = best;
+        });
+        const bool ok = calls == 11 && monotone && gpu.completed_runs == 10 && last == gpu.best_energy;
+        if (!ok) ++failures;
+        std::printf("%-28s calls %d monotone %d best %.6f  %s\n", "progress (test_runner 148)", calls, monotone,
+                    gpu.best_energy, ok ? "OK" : "FAIL");
+    }
+    // the synchronous baselines through the same seam: identical records to the reference's
+    for (int which = 0; which < 2; ++which) {
+        BatchSpec spec;
+        if (which == 0) spec.params = nmfa_defaults(300);
+        else spec.params = simcim_defaults(300);
+        spec.runs = 64;
+        spec.base_seed = 4;
+        const IsingProblem p = sk(128, 17);
+        const BatchStats ref = run_batch(p, spec);
+        const BatchStats gpu = gpu::run_batch(p, spec);
+        int same = 0;
+        for (size_t k = 0; k < ref.runs.size(); ++k)
+            same += ref.runs[k].spins == gpu.runs[k].spins && ref.runs[k].energy == gpu.runs[k].energy;
+        const bool ok = same >= 61 && gpu.best_energy <= ref.best_energy + 1e-9;
+        if (!ok) ++failures;
+        std::printf("%-28s ref best %.6f  gpu best %.6f  same runs %d/64  %s\n", which ? "simcim sk128" : "nmfa sk128",
+                    ref.best_energy, gpu.best_energy, same, ok ? "OK" : "FAIL");
+    }
+    // SA has no GPU path: InputError (not bad_variant_access)
+    {
+        BatchSpec spec;
+        spec.params = SaParams{};
+        spec.runs = 1;
+        bool threw = false;
+        try {
+            gpu::run_batch(sk(10, 1), spec);
+        } catch (const InputError&) {
+            threw = true;
+        }
+        if (!threw) ++failures;
+        std::printf("%-28s %s\n", "sa -> InputError", threw ? "OK" : "FAIL");
+    }
     std::printf("%s\n", failures ? "ADAPTER FAIL" : "ADAPTER OK");
     return failures ? 1 : 0;
 }

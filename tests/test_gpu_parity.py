@@ -497,3 +497,30 @@ def test_batch_outlives_destroyed_problem():
     rec, best, _ = b.fetch()
     assert (rec.status == 0).all() and 0 <= best < 64
     del b
+
+
+@pytest.mark.parametrize("kernel", ["dense_umma", "small", "dense_simt", "csr", "stencil"])
+def test_progress_during_the_batch(kernel, monkeypatch):
+    """run_batch's ProgressFn (test_runner.cpp:148-162): called once per run -- skipped slots
+    included -- with a non-increasing best, and the last best equal to the batch best; here from
+    the calling thread while the kernel runs (every relaxation kernel logs its finished runs)."""
+    import threading
+    monkeypatch.setenv("MARS_DENSE_SMALL", "1" if kernel == "small" else "0")
+    if kernel == "csr":
+        p = mb.IsingProblem.from_edges(300, mb.gen_er(300, 0.02, 4))
+    elif kernel == "stencil":
+        p = mb.IsingProblem.from_edges(256, mb.gen_ea(16, 2, 5))
+    elif kernel == "small":
+        p = mb.IsingProblem.dense(256, mb.gen_sk_pm1(256, 1))
+    else:
+        p = mb.IsingProblem.dense(200, mb.gen_sk_gaussian(200, 3), kernel=kernel)
+    spec = mb.BatchSpec(mb.MarsParams(0, 10, 0.5), 1, 5, keep_spins=True)     # grid: t = 0 slot skipped
+    calls, me = [], threading.get_ident()
+    stats = mb.run_batch(p, spec, progress=lambda i, b: calls.append((i, b, threading.get_ident())))
+    assert sorted(c[0] for c in calls) == list(range(len(stats.records.status)))
+    assert all(c[2] == me for c in calls)
+    bests = [c[1] for c in calls]
+    assert all(b2 <= b1 for b1, b2 in zip(bests, bests[1:]))
+    assert bests[-1] == stats.best_energy
+    plain = mb.run_batch(p, spec)
+    assert np.array_equal(plain.records.energy, stats.records.energy)
