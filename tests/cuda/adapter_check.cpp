@@ -3,6 +3,7 @@
 // per case: reference vs GPU best energy, identical-spin fraction, hit counts.
 #include <cmath>
 #include <cstdio>
+#include <limits>
 
 #include "mars/io.hpp"
 #include "mars/rng.hpp"
@@ -92,7 +93,7 @@ int main() {
         spec.base_seed = 2;
         int calls = 0;
         bool monotone = true;
-        double last = 1e300;
+        double last = std::numeric_limits<double>::infinity();   // test_runner.cpp:151
         const BatchStats gpu = gpu::run_batch(sk(10, 75), spec, [&](std::int64_t, double best) {
             ++calls;
             if (best > last + 1e-12) monotone = false;
