@@ -433,7 +433,7 @@ def run_b200(args, w, rank, world, local_rank, dist):
                    "total_runs": total_runs, "t_range": [0.0, w.t_max], "c_step": 1.0,
                    "d_min": 1e-4, "base_seed": w.base_seed,
                    "kernel": kname,
-                   "grid": timings[0]["grid"], "slots": timings[0]["slots"],
+                   "grid": timings[0]["grid"], "slots": timings[0]["slots"], "k_split": timings[0]["split"],
                    "l2": "flushed between timed steps (256 MB write); initial states %.0f MB" % (runs_per_gpu * w.n * s0_bytes / 1e6),
                    "parallelism": f"runs sharded over {world} GPU(s)", "note": w.note},
         "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,

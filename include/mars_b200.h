@@ -95,7 +95,7 @@ typedef struct {
     int32_t grid;            /* CTAs of the relaxation kernel                                */
     int32_t slots;           /* concurrent descents (run slots) on the device                */
     int32_t kernel;          /* relaxation kernel this batch ran: MARS_KERNEL_* or 4 = small  */
-    int32_t reserved;
+    int32_t split;           /* tcgen05 kernel: CTA pairs per 256-run tile (K split), else 1  */
 } mars_timing_t;
 
 typedef struct mars_problem mars_problem_t;

@@ -53,7 +53,7 @@ class mars_stats_t(C.Structure):
 class mars_timing_t(C.Structure):
     _fields_ = [("relax_ms", C.c_double), ("energy_ms", C.c_double), ("reduce_ms", C.c_double),
                 ("total_ms", C.c_double), ("launches", C.c_int64), ("total_sweeps", C.c_int64),
-                ("grid", C.c_int32), ("slots", C.c_int32), ("kernel", C.c_int32), ("reserved", C.c_int32)]
+                ("grid", C.c_int32), ("slots", C.c_int32), ("kernel", C.c_int32), ("split", C.c_int32)]
 
 
 class mars_nmfa_params_t(C.Structure):

@@ -95,6 +95,8 @@ struct UmmaLaunch {
     __half* s_hi;
     __half* s_lo;
     bool jlo;   // Gaussian couplings need the J_lo product; integer ones are exact in J_hi
+    int split;  // 1, or 2: two CTA pairs per 256-run tile split the K range (large N)
+    float* xpart;  // split 2: partial-field exchange [2][tile rows][128] fp32
 };
 cudaError_t launch_relax_dense_umma(const RelaxArgs& a, const UmmaLaunch& u, int grid, cudaStream_t st);
 int relax_dense_umma_slots_per_cta();

@@ -603,6 +603,7 @@ struct mars_batch {
     double* d_elapsed = nullptr;
     unsigned long long* d_done = nullptr;  // [count] retirement %globaltimer (time-to-best)
     double* d_failT = nullptr;             // [count] level temperature of a Diverged run
+    float* d_xpart = nullptr;              // split-K partial-field exchange (dense tcgen05)
     std::int8_t* d_spins = nullptr;
     double* d_energy = nullptr;
     double* d_cut = nullptr;
@@ -629,7 +630,7 @@ struct mars_batch {
             p->give(h, true);
         for (void* d : {d_s0, static_cast<void*>(d_temp), static_cast<void*>(d_order), d_work,
                         static_cast<void*>(d_queue), static_cast<void*>(d_status), static_cast<void*>(d_iters),
-                        static_cast<void*>(d_elapsed), static_cast<void*>(d_done), static_cast<void*>(d_failT), static_cast<void*>(d_spins), static_cast<void*>(d_energy),
+                        static_cast<void*>(d_elapsed), static_cast<void*>(d_done), static_cast<void*>(d_failT), static_cast<void*>(d_xpart), static_cast<void*>(d_spins), static_cast<void*>(d_energy),
                         static_cast<void*>(d_cut), static_cast<void*>(d_part_e), static_cast<void*>(d_part_i),
                         static_cast<void*>(d_best)})
             p->give(d, false);
@@ -875,17 +876,35 @@ int batch_alloc(mars_batch* b) {
         }
     }
     b->grid = std::max(1, std::min(max_grid, (b->queue_len + tm - 1) / tm));
-    if (p->kernel == MARS_KERNEL_DENSE_UMMA && !b->use_small)
+    int split = 1;
+    if (p->kernel == MARS_KERNEL_DENSE_UMMA && !b->use_small) {
         b->grid = std::max(2, b->grid + (b->grid & 1));   // CTA pairs (cta_group::2)
+        // Split-K for large N: the field GEMM of a block (K = N) dwarfs its walk, and a batch
+        // of few 256-run tiles would leave most SMs idle -- two CTA pairs per tile, each taking
+        // half of K, when the doubled grid still fits (cfg5: 8192 runs -> 128 CTAs).
+        // MARS_UMMA_SPLIT=1/2 forces.
+        const int se = env_int("MARS_UMMA_SPLIT", -1);
+        const bool want = se == 2 || (se < 0 && p->np >= 8192);
+        if (want && 2 * b->grid <= p->num_sms && (p->np / relax_dense_umma_kc()) % 2 == 0) split = 2;
+        b->umma.split = split;
+        b->grid *= split;
+    }
     b->sparse.grid = b->grid;
     b->spmm.grid = b->grid;
     b->stencil.grid = b->grid;
-    b->slots = b->grid * tm;
-    b->work_bytes = per_cta * b->grid;
+    b->slots = b->grid / split * tm;
+    b->work_bytes = per_cta * (b->grid / split);
     if (!(b->d_work = static_cast<decltype(b->d_work)>(p->take(std::max<std::size_t>(b->work_bytes, 16), false))))
         return fail(MARS_ERR_CUDA, "device allocation failed");
     if (p->kernel == MARS_KERNEL_DENSE_UMMA && !b->use_small) {
-        const std::size_t rows = relax_dense_umma_plane_rows(b->grid);
+        const std::size_t rows = relax_dense_umma_plane_rows(b->grid / split);
+        b->umma.xpart = nullptr;
+        if (split > 1) {
+            const std::size_t bytes = static_cast<std::size_t>(split - 1) * 2 * rows * relax_dense_umma_block() * sizeof(float);
+            if (!(b->d_xpart = static_cast<float*>(p->take(bytes, false))))
+                return fail(MARS_ERR_CUDA, "device allocation failed");
+            b->umma.xpart = b->d_xpart;
+        }
         b->umma.s_hi = static_cast<__half*>(b->d_work);
         b->umma.s_lo = b->umma.s_hi + rows * p->np;
         b->umma.tm_jhi = p->tm_jhi;
@@ -1484,7 +1503,7 @@ int execute_impl(mars_batch_t* b, mars_timing_t* timing, int fixed_sweeps, float
         if (p->kernel == MARS_KERNEL_DENSE_UMMA && !b->use_small)
             std::fprintf(stderr,
                          "[mars prof] grid %d: sweeps/cta %.1f, cycles/cta %.3g | per block, walker: turnover %.0f, "
-                         "wait jready+tmem_full %.0f, wait fields+ld %.0f, apply %.0f, walk %.0f, store/arrive %.0f | "
+                         "wait jready+tmem_full %.0f, wait fields+ld %.0f, old-state load %.0f, walk %.0f, store/arrive %.0f | "
                          "helper: wait tmem_full %.0f, work %.0f, wait deltas %.0f | producer wait ready %.0f empty %.0f | "
                          "mma wait full %.0f tmem_empty %.0f\n",
                          b->grid, acc[0] / b->grid, acc[1] / b->grid, acc[7] / blocks, acc[2] / blocks, acc[3] / blocks,
@@ -1504,6 +1523,7 @@ int execute_impl(mars_batch_t* b, mars_timing_t* timing, int fixed_sweeps, float
         timing->grid = b->grid;
         timing->slots = b->slots;
         timing->kernel = b->use_small ? 4 : p->kernel;
+        timing->split = (p->kernel == MARS_KERNEL_DENSE_UMMA && !b->use_small) ? std::max(1, b->umma.split) : 1;
         std::vector<long long> it(static_cast<std::size_t>(b->count));
         std::vector<std::uint8_t> stt(static_cast<std::size_t>(b->count));
         if (b->count) {

@@ -93,6 +93,7 @@ struct __align__(8) Ctl {
     std::uint64_t tmem_full[2];
     std::uint64_t tmem_empty[2];
     std::uint64_t chunk_ready[2];   // per 64-spin half block: walker write-back done
+    std::uint64_t part_ready[2];    // split-K: the other pairs' partial fields of a block in L2
     std::uint64_t jready[2];        // diagonal triangle staged (per smem buffer)
     std::uint64_t fready[4][2];     // helper -> walker: pre-corrected fields (per lane quarter)
     std::uint64_t dready[4][2];     // walker -> helper: a sub-block's Deltas in TMEM
@@ -134,6 +135,7 @@ __device__ __forceinline__ bool epi_any(bool v) {
 }
 
 struct UmmaParams {
+    float* xpart;            // split-K: partial fields of pairs 1.. [split-1][2][tile rows][TB] fp32
     const __half* s_hi;      // state planes (generic pointers for the epilogue)
     __half* s_hi_w;
     __half* s_lo_w;
@@ -281,6 +283,27 @@ __device__ __forceinline__ void walk_dispatch(float2 (&p)[SB / 2], float2 (&an)[
 
 // fields (fp32 pairs) += J[j0 .. j0+16)[col .. col+16)^T * d[0..16): the 16 x 16 rectangle
 // coupling one sub-block's Deltas to a later sub-block's fields (rows from the triangle)
+// split-K: the other pairs' partial fields (same prescaled units as the TMEM accumulator) for
+// 16 columns of this slot's row; L2 loads (written by other SMs this block)
+template <int SPLIT>
+__device__ __forceinline__ void add_partials(float (&pv)[16], const float* xpart, std::size_t plane, int buf,
+                                             std::size_t row, int col) {
+    if constexpr (SPLIT > 1) {
+#pragma unroll
+        for (int p = 0; p < SPLIT - 1; ++p) {
+            const float4* src = reinterpret_cast<const float4*>(xpart + ((p * 2 + buf) * plane + row) * TB + col);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const float4 x = __ldcg(src + v);
+                pv[4 * v] += x.x;
+                pv[4 * v + 1] += x.y;
+                pv[4 * v + 2] += x.z;
+                pv[4 * v + 3] += x.w;
+            }
+        }
+    }
+}
+
 template <int J>
 __device__ __forceinline__ void rect_row(float2 (&pf)[SB / 2], const TriRows& tr, int col, float d) {
     const float4* jr = reinterpret_cast<const float4*>(tr.template row<J>(col));
@@ -401,7 +424,11 @@ __device__ __forceinline__ bool pair_any(Ctl& ctl, bool local, bool lead, std::u
     return ctl.more_all != 0;
 }
 
-template <bool JLO>
+// SPLIT > 1 (large N): a cluster of 2*SPLIT CTAs = SPLIT pairs on the SAME 256 runs; pair p runs
+// the GEMM over the K chunks [p*nk/SPLIT, (p+1)*nk/SPLIT) and pairs 1.. export their partial
+// fields through L2 to pair 0, whose walkers and helpers add them (fp32) to their own before
+// the walk.  Only pair 0 owns run slots; the other pairs' producers follow its write-backs.
+template <bool JLO, int SPLIT>
 __global__ void __launch_bounds__(NT, 1)
 relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUtensorMap tm_shi,
                         const __grid_constant__ CUtensorMap tm_slo,
@@ -415,7 +442,12 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int np = a.np, n = a.n, nb = up.nb, nk = np / KC;
-    const int row0 = blockIdx.x * TM;
+    const std::uint32_t rank = cluster_ctarank();
+    const int pair = static_cast<int>(rank >> 1), half = static_cast<int>(rank & 1);
+    const bool leader = half == 0;
+    const int tile = blockIdx.x / (2 * SPLIT);
+    const int row0 = (2 * tile + half) * TM;             // this CTA's 128 state rows
+    const int c_lo = pair * (nk / SPLIT), c_hi = c_lo + nk / SPLIT;   // this pair's K chunks
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -427,6 +459,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
             mbar_init(&ctl.tmem_empty[s], 2 * NW);   // leader's: both CTAs' walkers
             mbar_init(&ctl.pair_more[s], 1);
             mbar_init(&ctl.chunk_ready[s], NW);
+            mbar_init(&ctl.part_ready[s], NW * (SPLIT - 1) + (SPLIT == 1));
             mbar_init(&ctl.jready[s], NW);
         }
         for (int q = 0; q < 4; ++q)
@@ -439,9 +472,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         ctl.poison = 0;
         fence_mbar_init();
     }
-    const std::uint32_t rank = cluster_ctarank();
-    const bool leader = rank == 0;
-    cluster_sync_all();                      // the peer's barriers exist before any remote arrive
+    cluster_sync_all();                      // the peers' barriers exist before any remote arrive
     if (warp == 1) tmem_alloc_pair(&ctl.tmem_base, TMEM_COLS);
     tc_fence_before();
     __syncthreads();
@@ -473,11 +504,12 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     if ((j == nk - CPB || j == nk - CPB / 2) && g > 0) {
                         // the last chunks of GEMM(b) are block b-1: wait for the walker's
                         // write-back of that half block (one barrier per 64-spin half)
-                        const int half = j == nk - CPB ? 0 : 1;
+                        const int hb = j == nk - CPB ? 0 : 1;
                         const long long t0 = clock64();
-                        mbar_wait(&ctl.chunk_ready[half], (g - 1) & 1);
+                        if (SPLIT > 1) mbar_wait_cluster(&ctl.chunk_ready[hb], (g - 1) & 1);
+                        else mbar_wait(&ctl.chunk_ready[hb], (g - 1) & 1);
                         w_ready += clock64() - t0;
-                        if (half == 1 && ctl.stop) {
+                        if (hb == 1 && ctl.stop) {
                             mbar_wait(&ctl.empty[s], ph ^ 1);
                             if (lane == 0) {
                                 if (leader) {
@@ -492,6 +524,10 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                             goto producer_done;
                         }
                     }
+                    if (c < c_lo || c >= c_hi) {             // another pair's K range
+                        if (++c == nk) c = 0;
+                        continue;
+                    }
                     const long long t1 = clock64();
                     mbar_wait(&ctl.empty[s], ph ^ 1);
                     w_empty += clock64() - t1;
@@ -502,8 +538,8 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     tma_load_2d_pair_elect(st + TILE_A, &tm_slo, fb, c * KC, row0, spol);
                     // the coupling tiles are read by every CTA every sweep: keep them in L2
                     // ahead of the per-CTA state planes; this CTA's half of the block's rows
-                    tma_load_2d_pair_elect(st + 2 * TILE_A, &tm_jhi, fb, c * KC, b * TB + rank * TBH, jpol);
-                    if (JLO) tma_load_2d_pair_elect(st + 2 * TILE_A + TILE_J, &tm_jlo, fb, c * KC, b * TB + rank * TBH, jpol);
+                    tma_load_2d_pair_elect(st + 2 * TILE_A, &tm_jhi, fb, c * KC, b * TB + half * TBH, jpol);
+                    if (JLO) tma_load_2d_pair_elect(st + 2 * TILE_A + TILE_J, &tm_jlo, fb, c * KC, b * TB + half * TBH, jpol);
                     if (up.pf > 0) {
                         // warm L2 with this CTA's state tiles up.pf chunks ahead (same block;
                         // a chunk of block b-1 fetched early is refreshed in L2 by the walker's
@@ -542,12 +578,14 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 w_tmem += clock64() - t0;
                 tc_fence_after();
                 const std::uint32_t d = tmem + buf * TB;
-                for (int j = 0; j < nk; ++j) {
+                for (int j = 0, c = b * CPB, cnt = 0; j < nk; ++j, c = c + 1 == nk ? 0 : c + 1) {
+                    if (c < c_lo || c >= c_hi) continue;    // another pair's K range
                     const long long t1 = clock64();
                     mbar_wait(&ctl.full[s], ph);
                     w_full += clock64() - t1;
-                    // the producer can only stop at the second write-back wait of a block
-                    if (j == nk - CPB / 2 && ctl.poison) {
+                    // the producer stops only at the second write-back wait of a block; it then
+                    // arrives on the next stage without data
+                    if ((SPLIT > 1 || j == nk - CPB / 2) && ctl.poison) {
                         if (a.prof && lane == 0) {
                             a.prof[blockIdx.x * kProfSlots + 10] = w_full;
                             a.prof[blockIdx.x * kProfSlots + 11] = w_tmem;
@@ -561,28 +599,61 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         const std::uint64_t ahi = desc_k_sw64(st + kk * 32);
                         const std::uint64_t alo = desc_k_sw64(st + TILE_A + kk * 32);
                         const std::uint64_t jhi = desc_k_sw64(st + 2 * TILE_A + kk * 32);
-                        mma_f16_ss_pair_elect(d, ahi, jhi, idesc, (j | kk) != 0);
+                        mma_f16_ss_pair_elect(d, ahi, jhi, idesc, (cnt | kk) != 0);
                         mma_f16_ss_pair_elect(d, alo, jhi, idesc, 1);
                         if (JLO) {
                             const std::uint64_t jlo = desc_k_sw64(st + 2 * TILE_A + TILE_J + kk * 32);
                             mma_f16_ss_pair_elect(d, ahi, jlo, idesc, 1);
                         }
                     }
-                    mma_commit_pair_mc_elect(&ctl.empty[s]);
+                    mma_commit_pair_mc_elect(&ctl.empty[s], pair);
+                    ++cnt;
                     if (++s == STAGES) {
                         s = 0;
                         ph ^= 1;
                     }
                 }
-                mma_commit_pair_mc_elect(&ctl.tmem_full[buf]);
+                mma_commit_pair_mc_elect(&ctl.tmem_full[buf], pair);
             }
         }
     mma_done:
-        mma_commit_pair_mc_elect(&ctl.mma_done);
+        mma_commit_pair_mc_elect(&ctl.mma_done, pair);
         mbar_wait(&ctl.mma_done, 0);
         }
     mma_skip:
         __syncwarp();
+    } else if (SPLIT > 1 && pair > 0) {
+        // ================================================================ exporters (split-K)
+        // Pairs 1..: the walker warps hand this pair's partial fields of every block to pair 0
+        // through L2; the helper warps have nothing to do.
+        if (warp < EPI_H) {
+            const int q = warp & 3;
+            const int r = q * 32 + lane;
+            const std::uint32_t lane_t = static_cast<std::uint32_t>(q * 32) << 16;
+            const std::size_t plane = static_cast<std::size_t>(gridDim.x / (2 * SPLIT)) * 2 * TM;
+            const std::uint32_t tmem_empty_leader = mapa_shared(smem_u32(&ctl.tmem_empty[0]), 2 * pair);
+            const std::uint32_t part_ready0 = mapa_shared(smem_u32(&ctl.part_ready[0]), half);
+            for (std::uint32_t g = 0;; ++g) {
+                const int buf = g & 1;
+                while (!mbar_try_wait(&ctl.tmem_full[buf], (g >> 1) & 1))
+                    if (ctl.stop) goto exporter_done;
+                tc_fence_after();
+                float* dst = up.xpart + (((pair - 1) * 2 + buf) * plane + row0 + r) * static_cast<std::size_t>(TB);
+#pragma unroll 1
+                for (int cc = 0; cc < TB / 16; ++cc) {
+                    float v[16];
+                    tmem_ld16(tmem + lane_t + buf * TB + cc * 16, v);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        __stcg(reinterpret_cast<float4*>(dst + cc * 16) + k,
+                               make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
+                }
+                tc_fence_before();
+                mbar_arrive_cluster(part_ready0 + buf * 8);           // pair 0, same half
+                mbar_arrive_cluster(tmem_empty_leader + buf * 8);     // this pair's leader MMA
+            }
+        exporter_done:;
+        }
     } else if (warp < EPI_H) {
         // ================================================================ walkers (W)
         // Warp w owns the runs of TMEM lane quarter q = w % 4 (slot r = 32q + lane) and walks
@@ -604,6 +675,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         bool quench = false;
         std::uint32_t g = 0, fe = 0, de = 0;                // block, F-event and D-event counters
         const std::uint32_t tmem_empty_leader = mapa_shared(smem_u32(&ctl.tmem_empty[0]), 0);
+        const std::size_t xplane = static_cast<std::size_t>(gridDim.x / (2 * SPLIT)) * 2 * TM;
         long long c_wait = 0, c_f = 0, c_apply = 0, c_walk = 0, c_turn = 0, c_st = 0, n_sweeps = 0;
         const long long c_start = clock64();
 
@@ -651,6 +723,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 fetch_old16(hi_row + b0, lo_row + b0, pre);
                 mbar_wait(&ctl.jready[buf], (g >> 1) & 1);
                 mbar_wait(&ctl.tmem_full[buf], (g >> 1) & 1);
+                if (SPLIT > 1) mbar_wait_cluster(&ctl.part_ready[buf], (g >> 1) & 1);
                 tc_fence_after();
                 t0 = clock64();
                 c_wait += t0 - t1;
@@ -662,10 +735,12 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 for (int j = 0; j < SB / 2; ++j) an[j] = make_float2(0.0f, 0.0f);
                 for (int t = 0; t < nsub; ++t) {
                     const int k0 = t * SB;
+                    const long long tpre = clock64();
                     float old[SB];
                     unpack_old16(pre, old);
                     if (t + 1 < nsub) fetch_old16(hi_row + b0 + k0 + SB, lo_row + b0 + k0 + SB, pre);
                     t1 = clock64();
+                    c_apply += t1 - tpre;                       // the old-state load wait
                     if (t >= 2) {
                         mbar_wait(&ctl.fready[q][fe & 1], (fe >> 1) & 1);
                         ++fe;
@@ -673,6 +748,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     }
                     float pv[SB];
                     tmem_ld16(tacc + k0, pv);
+                    if (t < 2) add_partials<SPLIT>(pv, up.xpart, xplane, buf, row0 + r, k0);
                     // raw GEMM fields (t < 2) are on the prescaled couplings; the helper's are not
                     const float sc = t >= 2 ? 1.0f : a.jscale;
                     float2 pf[SB / 2];
@@ -703,6 +779,8 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         // first 64-spin chunk of this block written back: its GEMM chunk may go
                         fence_proxy_async_global();
                         mbar_arrive(&ctl.chunk_ready[0]);
+                        for (int p = 1; p < SPLIT; ++p)
+                            mbar_arrive_cluster(mapa_shared(smem_u32(&ctl.chunk_ready[0]), 2 * p + half));
                     }
                     c_st += clock64() - t0;
                 }
@@ -733,13 +811,20 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     Tf = static_cast<float>(slot.T);
                     rT = quench ? 0.0f : recip_for_div(Tf);
                     const bool more = pair_any(ctl, epi_any(mode != kIdle), wt == 0, rank, n_sweeps - 1);
-                    if (!more && wt == 0) ctl.stop = 1;
+                    if (!more && wt == 0) {
+                        ctl.stop = 1;
+                        for (int p = 1; p < SPLIT; ++p) st_cluster_u32(mapa_shared(smem_u32(const_cast<std::uint32_t*>(&ctl.stop)), 2 * p + half), 1u);
+                    }
                     fence_proxy_async_global();
                     mbar_arrive(&ctl.chunk_ready[1]);
+                    for (int p = 1; p < SPLIT; ++p)
+                        mbar_arrive_cluster(mapa_shared(smem_u32(&ctl.chunk_ready[1]), 2 * p + half));
                     if (!more) goto walker_done;
                 } else {
                     fence_proxy_async_global();
                     mbar_arrive(&ctl.chunk_ready[1]);
+                    for (int p = 1; p < SPLIT; ++p)
+                        mbar_arrive_cluster(mapa_shared(smem_u32(&ctl.chunk_ready[1]), 2 * p + half));
                 }
             }
         }
@@ -767,6 +852,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         const std::uint32_t lane_t = static_cast<std::uint32_t>(q * 32) << 16;
         std::uint32_t g = 0, fe = 0, de = 0;
         long long c_dw = 0, c_work = 0, c_tw = 0, h_sweeps = 0;
+        const std::size_t xplane = static_cast<std::size_t>(gridDim.x / (2 * SPLIT)) * 2 * TM;
         issue_jtri(Jtri0, a.J32, np, 0, ht);
         cp_async_arrive_noinc(&ctl.jready[0]);
         for (;;) {
@@ -779,6 +865,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 long long t0 = clock64();
                 mbar_wait(&ctl.jready[buf], (g >> 1) & 1);
                 mbar_wait(&ctl.tmem_full[buf], (g >> 1) & 1);
+                if (SPLIT > 1) mbar_wait_cluster(&ctl.part_ready[buf], (g >> 1) & 1);
                 tc_fence_after();
                 long long t1 = clock64();
                 c_tw += t1 - t0;
@@ -793,6 +880,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     if (target) {
                         float pv[SB];
                         tmem_ld16(tacc + t * SB, pv);
+                        add_partials<SPLIT>(pv, up.xpart, xplane, buf, row0 + (q * 32 + lane), t * SB);
 #pragma unroll
                         for (int j = 0; j < SB / 2; ++j) pf[j] = make_float2(pv[2 * j] * a.jscale, pv[2 * j + 1] * a.jscale);
                         // Deltas already final: sub-blocks 0 .. t-3
@@ -868,10 +956,12 @@ std::size_t relax_dense_umma_plane_rows(int grid) { return static_cast<std::size
 
 cudaError_t launch_relax_dense_umma(const RelaxArgs& a, const UmmaLaunch& u, int grid, cudaStream_t st) {
     const char* pf = std::getenv("MARS_UMMA_PF");
-    UmmaParams up{u.s_hi, u.s_hi, u.s_lo, a.np / TB, pf ? std::atoi(pf) : 0};
-    if (a.np % TB != 0 || grid % 2 != 0) return cudaErrorInvalidValue;
-    void (*kern)(RelaxArgs, UmmaParams, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap) =
-        u.jlo ? relax_dense_umma_kernel<true> : relax_dense_umma_kernel<false>;
+    UmmaParams up{u.xpart, u.s_hi, u.s_hi, u.s_lo, a.np / TB, pf ? std::atoi(pf) : 0};
+    const int split = u.split > 1 ? 2 : 1;
+    if (a.np % TB != 0 || grid % (2 * split) != 0 || (a.np / KC) % split != 0) return cudaErrorInvalidValue;
+    using K = void (*)(RelaxArgs, UmmaParams, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap);
+    K kern = split == 1 ? (u.jlo ? relax_dense_umma_kernel<true, 1> : relax_dense_umma_kernel<false, 1>)
+                        : (u.jlo ? relax_dense_umma_kernel<true, 2> : relax_dense_umma_kernel<false, 2>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
@@ -880,8 +970,8 @@ cudaError_t launch_relax_dense_umma(const RelaxArgs& a, const UmmaLaunch& u, int
     cfg.dynamicSmemBytes = SMEM_TOTAL;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;        // the cta_group::2 pair
-    attr[0].val.clusterDim.x = 2;
+    attr[0].id = cudaLaunchAttributeClusterDimension;        // split CTA pairs (cta_group::2)
+    attr[0].val.clusterDim.x = 2 * split;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;

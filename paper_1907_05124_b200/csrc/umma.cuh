@@ -410,14 +410,15 @@ __device__ __forceinline__ void mma_f16_ss_pair_elect(std::uint32_t d_tmem, std:
         : "memory");
 }
 
-// commit the pair's MMAs to the barrier at the same offset in both CTAs
-__device__ __forceinline__ void mma_commit_pair_mc_elect(std::uint64_t* bar) {
+// commit the pair's MMAs to the barrier at the same offset in both CTAs of pair `pair` of the
+// cluster (ranks 2*pair, 2*pair + 1)
+__device__ __forceinline__ void mma_commit_pair_mc_elect(std::uint64_t* bar, int pair = 0) {
+    const std::uint16_t mask = static_cast<std::uint16_t>(3u << (2 * pair));
     asm volatile(
-        "{\n\t.reg .pred p;\n\t.reg .b16 m;\n\t"
-        "mov.b16 m, 3;\n\t"
+        "{\n\t.reg .pred p;\n\t"
         "elect.sync _|p, 0xffffffff;\n\t"
-        "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}\n" ::"r"(
-            smem_u32(bar))
+        "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
+            smem_u32(bar)), "h"(mask)
         : "memory");
 }
 

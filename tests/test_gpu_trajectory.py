@@ -49,18 +49,22 @@ def _states(g, name, n):
     return np.stack([mb.initial_state(int(s), n) for s in g[name + "_seeds"]]).astype(np.float32)
 
 
-@pytest.mark.parametrize("name,kernel,small", [
-    ("pm256", "dense_umma", "0"),     # tcgen05 kernel
-    ("pm256", "dense_umma", "1"),     # warp-per-run on-chip kernel (relax_small.cu)
-    ("pm256", "dense_simt", None),    # CUDA-core blocked kernel
-    ("sk2000", "dense_umma", None),
-    ("sk2000", "dense_simt", None),
-    ("sk16384", "dense_umma", None),
+@pytest.mark.parametrize("name,kernel,small,split", [
+    ("pm256", "dense_umma", "0", None),     # tcgen05 kernel
+    ("pm256", "dense_umma", "0", "2"),      # tcgen05, K split over two CTA pairs
+    ("pm256", "dense_umma", "1", None),     # warp-per-run on-chip kernel (relax_small.cu)
+    ("pm256", "dense_simt", None, None),    # CUDA-core blocked kernel
+    ("sk2000", "dense_umma", None, None),
+    ("sk2000", "dense_umma", None, "2"),
+    ("sk2000", "dense_simt", None, None),
+    ("sk16384", "dense_umma", None, None),  # N >= 8192: split over two pairs by default
 ])
-def test_single_sweep_matches_reference(name, kernel, small, monkeypatch):
+def test_single_sweep_matches_reference(name, kernel, small, split, monkeypatch):
     g = golden("sweeps")
     if small is not None:
         monkeypatch.setenv("MARS_DENSE_SMALL", small)
+    if split is not None:
+        monkeypatch.setenv("MARS_UMMA_SPLIT", split)
     n, J = _instance(name)
     p = mb.IsingProblem.dense(n, J, kernel=kernel)
     s0 = _states(g, name, n)
@@ -159,3 +163,23 @@ def test_fp32_replay_fixture_is_consistent():
     r = golden("cfg2_sk2000_f32replay")
     g = golden("cfg2_sk2000_prefix")
     assert len(r["status"]) == len(g["status"]) and np.array_equal(r["status"], g["status"])
+
+
+@pytest.mark.parametrize("split", ["1", "2"])
+def test_split_k_batches_match_reference(split, monkeypatch):
+    """The split-K tcgen05 path (two CTA pairs per 256-run tile, partial fields through L2) on
+    whole batches: cfg1's instance against the reference's full batch (best energy exact, >= 98%
+    identical spins) and the first 256 cfg2 descents against the fp32 floor."""
+    from test_gpu_parity import SPIN_FRACTION, compare_records, fp32_floor_gate
+    monkeypatch.setenv("MARS_DENSE_SMALL", "0")
+    monkeypatch.setenv("MARS_UMMA_SPLIT", split)
+    w = WORKLOADS["cfg1_sk256_pm1"]
+    stats = mb.run_batch(build_problem(w), mb.BatchSpec(w.params(), w.runs, w.base_seed, keep_spins=True))
+    compare_records(stats, golden("cfg1"), w.n, frac=SPIN_FRACTION)
+    assert stats.best_energy == -6120.0
+    g = golden("cfg2_sk2000_prefix")
+    w = WORKLOADS["cfg2_sk2000"]
+    rec = mb.run_shard(build_problem(w), mb.BatchSpec(w.params(), w.runs, w.base_seed, keep_spins=True), 0, 256)
+    same = np.all(rec.spins == unpack_spins(g["spins_packed"], w.n)[:256], axis=1)
+    assert same.mean() >= fp32_floor_gate(256), same.mean()
+    assert np.array_equal(rec.energy[same], g["energy"][:256][same])
