@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmars_b200.so")
+# MARS_B200_LIB names an alternative build next to this file (A/B kernel experiments)
+LIB_PATH = os.path.join(HERE, os.path.basename(os.environ.get("MARS_B200_LIB") or "libmars_b200.so"))
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with "

@@ -15,6 +15,10 @@ namespace marsb200 {
 // sets mars_last_error() on the calling thread, returns `code`
 int host_fail(int code, const std::string& msg);
 
+// "; mbarrier wait timed out in block .. thread .. (smem .., parity ..)" once the tcgen05
+// kernel's hang detector has fired in this process, else ""
+std::string hang_note();
+
 // Device-resident records of an executed batch (mars_batch_execute), shard-local indexing.
 struct BatchDevView {
     int device;

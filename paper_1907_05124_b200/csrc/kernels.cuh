@@ -104,6 +104,8 @@ int relax_dense_umma_block();
 int relax_dense_umma_kc();      // K per pipeline stage (the TMA box width of both operand maps)
 int relax_dense_umma_j_rows();  // coupling-tile rows per CTA of the pair (TMA box height of J maps)
 std::size_t relax_dense_umma_plane_rows(int grid);
+int relax_dense_umma_max_clusters(int split, bool jlo);   // resident clusters of 2*split CTAs
+cudaError_t relax_dense_umma_hang_log(unsigned long long** host);   // host view of the hang record
 
 // Synchronous mean-field baselines on tcgen05 (jacobi_umma.cu): NMFA (solver 0) and SimCIM
 // (solver 1), solvers.cpp:374-443.  CTA pairs (grid even); 128 runs per CTA per tile round.

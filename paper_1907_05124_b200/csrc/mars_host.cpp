@@ -40,11 +40,14 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 
-#define CUDA_TRY(expr)                                                                     \
-    do {                                                                                   \
-        const cudaError_t e_ = (expr);                                                     \
-        if (e_ != cudaSuccess)                                                             \
-            return fail(MARS_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+// an asynchronous kernel fault surfaces at whichever call comes next: the tcgen05 kernel's
+// hang-detector record (if it fired) is appended to the message
+#define CUDA_TRY(expr)                                                                                  \
+    do {                                                                                                \
+        const cudaError_t e_ = (expr);                                                                  \
+        if (e_ != cudaSuccess)                                                                          \
+            return fail(MARS_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_) +               \
+                                           (e_ == cudaErrorLaunchFailure ? ::marsb200::hang_note() : "")); \
     } while (0)
 
 constexpr double kSparseDensityThreshold = 0.05;      // model.hpp:31
@@ -882,10 +885,21 @@ int batch_alloc(mars_batch* b) {
         // Split-K for large N: the field GEMM of a block (K = N) dwarfs its walk, and a batch
         // of few 256-run tiles would leave most SMs idle -- two CTA pairs per tile, each taking
         // half of K, when the doubled grid still fits (cfg5: 8192 runs -> 128 CTAs).
-        // MARS_UMMA_SPLIT=1/2 forces.
+        // MARS_UMMA_SPLIT=1/2/4 forces.
+        // Up to 4 pairs per tile (a cluster of 8) for small shards, e.g. the 1024-run share of
+        // an 8-GPU cfg5 run.
         const int se = env_int("MARS_UMMA_SPLIT", -1);
-        const bool want = se == 2 || (se < 0 && p->np >= 8192);
-        if (want && 2 * b->grid <= p->num_sms && (p->np / relax_dense_umma_kc()) % 2 == 0) split = 2;
+        const int nkc = p->np / relax_dense_umma_kc();
+        for (int cand : {4, 2})
+            if (split == 1 && (se == cand || (se < 0 && p->np >= 8192)) && cand * b->grid <= p->num_sms &&
+                nkc % cand == 0)
+                split = cand;
+        // the whole grid must be resident at once (one wave of clusters)
+        while (split > 1 && relax_dense_umma_max_clusters(split, p->jlo) < b->grid / 2) split /= 2;
+        if (std::getenv("MARS_UMMA_DEBUG"))
+            std::fprintf(stderr, "[mars umma] pairs %d split %d resident clusters %d/%d/%d (split 1/2/4)\n", b->grid / 2,
+                         split, relax_dense_umma_max_clusters(1, p->jlo), relax_dense_umma_max_clusters(2, p->jlo),
+                         relax_dense_umma_max_clusters(4, p->jlo));
         b->umma.split = split;
         b->grid *= split;
     }
@@ -922,6 +936,18 @@ int batch_alloc(mars_batch* b) {
 namespace marsb200 {
 
 int host_fail(int code, const std::string& msg) { return fail(code, msg); }
+
+// the tcgen05 kernel's hang detector record (umma.cuh), as text for an error message
+std::string hang_note() {
+    unsigned long long* h = nullptr;
+    if (relax_dense_umma_hang_log(&h) != cudaSuccess || !h) return "";
+    const volatile unsigned long long* v = h;
+    if (v[0] == 0) return "";
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "; mbarrier wait timed out in block %llu thread %llu (smem 0x%llx, parity %llu)",
+                  v[1], v[2], v[3], v[4]);
+    return buf;
+}
 
 int batch_device_view(mars_batch_t* b, BatchDevView* v) {
     if (!b || !v) return fail(MARS_ERR_INPUT, "null argument");
@@ -1463,6 +1489,11 @@ int execute_impl(mars_batch_t* b, mars_timing_t* timing, int fixed_sweeps, float
                          : b->use_spmm ? launch_relax_spmm(ra, sparse_levels(p), b->spmm, st)
                                        : launch_relax_sparse(ra, sparse_levels(p), b->sparse, st));
         ++launches;
+        if (std::getenv("MARS_SYNC_CHECK")) {          // attribute an asynchronous fault to the relaxation
+            const cudaError_t e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess)
+                return fail(MARS_ERR_CUDA, std::string("relaxation kernel: ") + cudaGetErrorString(e) + ::marsb200::hang_note());
+        }
     }
     if (prog) {
         if (b->queue_len > 0) {

@@ -48,6 +48,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstddef>
+#include <cstdio>
 #include <cstdlib>
 #include <utility>
 
@@ -92,7 +94,6 @@ struct __align__(8) Ctl {
     std::uint64_t empty[STAGES];
     std::uint64_t tmem_full[2];
     std::uint64_t tmem_empty[2];
-    std::uint64_t chunk_ready[2];   // per 64-spin half block: walker write-back done
     std::uint64_t part_ready[2];    // split-K: the other pairs' partial fields of a block in L2
     std::uint64_t jready[2];        // diagonal triangle staged (per smem buffer)
     std::uint64_t fready[4][2];     // helper -> walker: pre-corrected fields (per lane quarter)
@@ -102,8 +103,14 @@ struct __align__(8) Ctl {
     std::uint32_t peer_more[2];     // written remotely by the peer
     std::uint32_t more_all;
     std::uint32_t tmem_base;
-    volatile std::uint32_t stop;
-    volatile std::uint32_t poison;  // producer stopped: the stage it arrived on carries no data
+    // Write-back counters, per 64-spin half block: +1 per walker warp of pair 0 (same half)
+    // each time it has written that half of a block back (so 4*(g+1) after block g).  A
+    // monotonic count, not an mbarrier: with split-K a pair whose K range misses a block need
+    // not wait for it, so the walkers may be any number of blocks past such a pair's producer.
+    std::uint32_t wb[2];
+    volatile std::uint32_t stop;    // end of the batch (set by pair 0's walkers in every CTA)
+    volatile std::uint32_t poison;  // 1 + the sequence number of the stage the leader producer
+                                    // arrived on without data when it stopped (0 = running)
 };
 
 // dynamic smem: [stages: A_hi A_lo J_hi J_lo] [Jtri x 2: upper triangle of the diagonal block,
@@ -194,11 +201,6 @@ struct SubCtx {
 
 __device__ __forceinline__ float2 ffma2(float2 a, float b, float2 c) {
     return __ffma2_rn(a, make_float2(b, b), c);
-}
-
-// address of J[i][col], col >= tri_k0(i), inside the packed triangle
-__device__ __forceinline__ const float* tri_ptr(const float* jtri, int i, int col) {
-    return jtri + tri_row_off_rt(i) - tri_k0(i) + col;
 }
 
 
@@ -424,6 +426,29 @@ __device__ __forceinline__ bool pair_any(Ctl& ctl, bool local, bool lead, std::u
     return ctl.more_all != 0;
 }
 
+// a walker warp has written half `hb` of a block back: count it in this CTA and in the CTAs
+// of the other pairs on the same runs (same half).  Each lane's stores are ordered before the
+// producer's TMA reads by its proxy fence, the warp barrier and lane 0's release.
+template <int SPLIT>
+__device__ __forceinline__ void signal_writeback(Ctl& ctl, int hb, int half, int lane) {
+    fence_proxy_async_global();
+    __syncwarp();
+    if (lane == 0) {
+        red_add_release_cta(&ctl.wb[hb], 1u);
+        for (int p = 1; p < SPLIT; ++p) red_add_release_cluster(mapa_shared(smem_u32(&ctl.wb[hb]), 2 * p + half), 1u);
+    }
+}
+
+// wait until the write-back counter of half `hb` reaches `target` (4 per block written back)
+__device__ __forceinline__ void wait_writeback(Ctl& ctl, int hb, std::uint32_t target) {
+    if (ld_acquire_cluster(&ctl.wb[hb]) >= target) return;
+    std::uint64_t h0 = 0;
+    for (std::uint32_t spin = 1; ld_acquire_cluster(&ctl.wb[hb]) < target; ++spin) {
+        if (spin > 64) __nanosleep(32);
+        if (hang_check(h0, spin)) mbar_hang(&ctl.tmem_full[0], 0x100u + hb);   // (reported as 0x10h)
+    }
+}
+
 // SPLIT > 1 (large N): a cluster of 2*SPLIT CTAs = SPLIT pairs on the SAME 256 runs; pair p runs
 // the GEMM over the K chunks [p*nk/SPLIT, (p+1)*nk/SPLIT) and pairs 1.. export their partial
 // fields through L2 to pair 0, whose walkers and helpers add them (fp32) to their own before
@@ -458,7 +483,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
             mbar_init(&ctl.tmem_full[s], 1);
             mbar_init(&ctl.tmem_empty[s], 2 * NW);   // leader's: both CTAs' walkers
             mbar_init(&ctl.pair_more[s], 1);
-            mbar_init(&ctl.chunk_ready[s], NW);
+            ctl.wb[s] = 0;
             mbar_init(&ctl.part_ready[s], NW * (SPLIT - 1) + (SPLIT == 1));
             mbar_init(&ctl.jready[s], NW);
         }
@@ -471,6 +496,13 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         ctl.stop = 0;
         ctl.poison = 0;
         fence_mbar_init();
+        if (a.prof && blockIdx.x == 0)
+            printf("mars: relax_dense_umma Ctl at smem 0x%x (full +0, empty +%d, tmem_full +%d, tmem_empty +%d, "
+                   "wb +%d, part_ready +%d, jready +%d, fready +%d, dready +%d, mma_done +%d, pair_more +%d)\n",
+                   smem_u32(&ctl), int(offsetof(Ctl, empty)), int(offsetof(Ctl, tmem_full)), int(offsetof(Ctl, tmem_empty)),
+                   int(offsetof(Ctl, wb)), int(offsetof(Ctl, part_ready)), int(offsetof(Ctl, jready)),
+                   int(offsetof(Ctl, fready)), int(offsetof(Ctl, dready)), int(offsetof(Ctl, mma_done)),
+                   int(offsetof(Ctl, pair_more)));
     }
     cluster_sync_all();                      // the peers' barriers exist before any remote arrive
     if (warp == 1) tmem_alloc_pair(&ctl.tmem_base, TMEM_COLS);
@@ -495,25 +527,30 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         const std::uint32_t smem0 = smem_u32(base);
         const std::uint32_t full0 = smem_u32(&ctl.full[0]);
         const std::uint32_t tx = 2 * (JLO ? STAGE_BYTES : STAGE_BYTES - TILE_J);   // both CTAs' bytes
-        std::uint32_t g = 0, s = 0, ph = 0;
+        std::uint32_t g = 0, s = 0, ph = 0, seq = 0;   // seq: stages issued so far
         long long w_ready = 0, w_empty = 0;
         for (;;) {
             for (int b = 0; b < nb; ++b, ++g) {
                 int c = b * CPB;                               // chunk order: block b first
                 for (int j = 0; j < nk; ++j) {
-                    if ((j == nk - CPB || j == nk - CPB / 2) && g > 0) {
-                        // the last chunks of GEMM(b) are block b-1: wait for the walker's
-                        // write-back of that half block (one barrier per 64-spin half)
-                        const int hb = j == nk - CPB ? 0 : 1;
+                    const bool mine = c >= c_lo && c < c_hi;   // in this pair's K range
+                    // The last chunks of GEMM(b) are block b-1: a pair that reads them waits until
+                    // the walkers have written that half block back.  At GEMM(0) every pair waits
+                    // for the end of the previous sweep (block nb-1, second half): the walkers
+                    // raise `stop` before that write-back, so both producers of a pair stop at
+                    // this same point of their stage sequence.
+                    const bool sweep_end = b == 0 && j == nk - CPB / 2;
+                    if ((j == nk - CPB || j == nk - CPB / 2) && g > 0 && (mine || sweep_end)) {
                         const long long t0 = clock64();
-                        if (SPLIT > 1) mbar_wait_cluster(&ctl.chunk_ready[hb], (g - 1) & 1);
-                        else mbar_wait(&ctl.chunk_ready[hb], (g - 1) & 1);
+                        wait_writeback(ctl, j == nk - CPB ? 0 : 1, 4u * g);
                         w_ready += clock64() - t0;
-                        if (hb == 1 && ctl.stop) {
+                        if (sweep_end && ctl.stop) {
+                            // end of the batch: the next stage carries no data; the leader names
+                            // it for its MMA issuer, which consumes every stage before it
                             mbar_wait(&ctl.empty[s], ph ^ 1);
                             if (lane == 0) {
                                 if (leader) {
-                                    ctl.poison = 1;
+                                    ctl.poison = seq + 1;
                                     mbar_arrive(&ctl.full[s]);
                                 }
                                 if (a.prof) {
@@ -524,7 +561,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                             goto producer_done;
                         }
                     }
-                    if (c < c_lo || c >= c_hi) {             // another pair's K range
+                    if (!mine) {                              // another pair's K range
                         if (++c == nk) c = 0;
                         continue;
                     }
@@ -552,6 +589,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         }
                     }
                     if (++c == nk) c = 0;
+                    ++seq;
                     if (++s == STAGES) {
                         s = 0;
                         ph ^= 1;
@@ -568,7 +606,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         {
         constexpr std::uint32_t idesc = idesc_f16(2 * TM, TB, 0);
         const std::uint32_t smem0 = smem_u32(base);
-        std::uint32_t g = 0, s = 0, ph = 0;
+        std::uint32_t g = 0, s = 0, ph = 0, seq = 0;   // seq: stages consumed so far
         long long w_full = 0, w_tmem = 0;
         for (;;) {
             for (int b = 0; b < nb; ++b, ++g) {
@@ -583,9 +621,9 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     const long long t1 = clock64();
                     mbar_wait(&ctl.full[s], ph);
                     w_full += clock64() - t1;
-                    // the producer stops only at the second write-back wait of a block; it then
-                    // arrives on the next stage without data
-                    if ((SPLIT > 1 || j == nk - CPB / 2) && ctl.poison) {
+                    // the producers' stop point is the chunk at nk - CPB/2 of GEMM(0), or (a pair
+                    // whose K range ends before it) the first chunk of GEMM(1)
+                    if ((b == 0 ? j >= nk - CPB / 2 : b == 1 && cnt == 0) && ctl.poison == seq + 1) {
                         if (a.prof && lane == 0) {
                             a.prof[blockIdx.x * kProfSlots + 10] = w_full;
                             a.prof[blockIdx.x * kProfSlots + 11] = w_tmem;
@@ -608,6 +646,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     }
                     mma_commit_pair_mc_elect(&ctl.empty[s], pair);
                     ++cnt;
+                    ++seq;
                     if (++s == STAGES) {
                         s = 0;
                         ph ^= 1;
@@ -635,9 +674,15 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
             const std::uint32_t part_ready0 = mapa_shared(smem_u32(&ctl.part_ready[0]), half);
             for (std::uint32_t g = 0;; ++g) {
                 const int buf = g & 1;
-                while (!mbar_try_wait(&ctl.tmem_full[buf], (g >> 1) & 1))
+                std::uint64_t t0 = 0;
+                for (std::uint32_t spin = 1; !mbar_try_wait(&ctl.tmem_full[buf], (g >> 1) & 1); ++spin) {
                     if (ctl.stop) goto exporter_done;
+                    if (hang_check(t0, spin)) mbar_hang(&ctl.tmem_full[buf], (g >> 1) & 1);
+                }
                 tc_fence_after();
+                // xpart[buf] last held block g-2: pair 0 is done with it once its walkers are
+                // past that block (its helpers finish a block before its walkers do)
+                if (g >= 2) wait_writeback(ctl, 1, 4u * (g - 1));
                 float* dst = up.xpart + (((pair - 1) * 2 + buf) * plane + row0 + r) * static_cast<std::size_t>(TB);
 #pragma unroll 1
                 for (int cc = 0; cc < TB / 16; ++cc) {
@@ -777,10 +822,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     }
                     if (t == min(TB / 2 / SB, nsub) - 1) {
                         // first 64-spin chunk of this block written back: its GEMM chunk may go
-                        fence_proxy_async_global();
-                        mbar_arrive(&ctl.chunk_ready[0]);
-                        for (int p = 1; p < SPLIT; ++p)
-                            mbar_arrive_cluster(mapa_shared(smem_u32(&ctl.chunk_ready[0]), 2 * p + half));
+                        signal_writeback<SPLIT>(ctl, 0, half, lane);
                     }
                     c_st += clock64() - t0;
                 }
@@ -815,16 +857,10 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         ctl.stop = 1;
                         for (int p = 1; p < SPLIT; ++p) st_cluster_u32(mapa_shared(smem_u32(const_cast<std::uint32_t*>(&ctl.stop)), 2 * p + half), 1u);
                     }
-                    fence_proxy_async_global();
-                    mbar_arrive(&ctl.chunk_ready[1]);
-                    for (int p = 1; p < SPLIT; ++p)
-                        mbar_arrive_cluster(mapa_shared(smem_u32(&ctl.chunk_ready[1]), 2 * p + half));
+                    signal_writeback<SPLIT>(ctl, 1, half, lane);   // after `stop` (lane 0 of warp 2)
                     if (!more) goto walker_done;
                 } else {
-                    fence_proxy_async_global();
-                    mbar_arrive(&ctl.chunk_ready[1]);
-                    for (int p = 1; p < SPLIT; ++p)
-                        mbar_arrive_cluster(mapa_shared(smem_u32(&ctl.chunk_ready[1]), 2 * p + half));
+                    signal_writeback<SPLIT>(ctl, 1, half, lane);
                 }
             }
         }
@@ -946,6 +982,31 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
     if (warp == 1) tmem_dealloc_pair(tmem, TMEM_COLS);
 }
 
+using UmmaKernel = void (*)(RelaxArgs, UmmaParams, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap);
+
+UmmaKernel umma_kernel(int split, bool jlo) {
+    return split == 1   ? (jlo ? relax_dense_umma_kernel<true, 1> : relax_dense_umma_kernel<false, 1>)
+           : split == 2 ? (jlo ? relax_dense_umma_kernel<true, 2> : relax_dense_umma_kernel<false, 2>)
+                        : (jlo ? relax_dense_umma_kernel<true, 4> : relax_dense_umma_kernel<false, 4>);
+}
+
+int clamp_split(int split) { return split >= 4 ? 4 : (split >= 2 ? 2 : 1); }
+
+cudaLaunchConfig_t umma_config(int grid, int split, cudaStream_t st, cudaLaunchAttribute* attr) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = SMEM_TOTAL;
+    cfg.stream = st;
+    attr[0].id = cudaLaunchAttributeClusterDimension;        // split CTA pairs (cta_group::2)
+    attr[0].val.clusterDim.x = 2 * split;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cfg;
+}
+
 }  // namespace
 
 int relax_dense_umma_slots_per_cta() { return TM; }
@@ -954,28 +1015,62 @@ int relax_dense_umma_kc() { return KC; }
 int relax_dense_umma_j_rows() { return TBH; }
 std::size_t relax_dense_umma_plane_rows(int grid) { return static_cast<std::size_t>(grid) * TM; }
 
+// How many clusters of 2*split CTAs the device keeps resident at once: the persistent grid
+// must fit in one wave (a cluster's pairs wait on each other, and on nothing outside it, but
+// a cluster left for a second wave would start only after the whole first wave retired).
+int relax_dense_umma_max_clusters(int split, bool jlo) {
+    split = clamp_split(split);
+    UmmaKernel kern = umma_kernel(split, jlo);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL) != cudaSuccess) return -1;
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = umma_config(2 * split, split, nullptr, attr);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) return -1;
+    return n;
+}
+
+// The host-mapped hang record (umma.cuh) of this translation unit's kernels, allocated once
+// per process; *host receives the host view.
+cudaError_t relax_dense_umma_hang_log(unsigned long long** host) {
+    static unsigned long long* h = nullptr;
+    static int dev_set = -1;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (!h) {
+        if ((e = cudaHostAlloc(reinterpret_cast<void**>(&h), 8 * sizeof(unsigned long long),
+                               cudaHostAllocMapped | cudaHostAllocPortable)) != cudaSuccess) {
+            h = nullptr;
+            return e;
+        }
+        for (int i = 0; i < 8; ++i) h[i] = 0;
+    }
+    if (dev_set != dev) {
+        unsigned long long* d = nullptr;
+        if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), h, 0)) != cudaSuccess) return e;
+        if ((e = cudaMemcpyToSymbol(g_hang_log, &d, sizeof(d))) != cudaSuccess) return e;
+        if (const char* hs = std::getenv("MARS_HANG_S")) {
+            const unsigned long long ns = static_cast<unsigned long long>(std::atof(hs) * 1e9);
+            if ((e = cudaMemcpyToSymbol(g_hang_ns, &ns, sizeof(ns))) != cudaSuccess) return e;
+        }
+        dev_set = dev;
+    }
+    *host = h;
+    return cudaSuccess;
+}
+
 cudaError_t launch_relax_dense_umma(const RelaxArgs& a, const UmmaLaunch& u, int grid, cudaStream_t st) {
+    unsigned long long* hang = nullptr;
+    if (cudaError_t e = relax_dense_umma_hang_log(&hang)) return e;
     const char* pf = std::getenv("MARS_UMMA_PF");
     UmmaParams up{u.xpart, u.s_hi, u.s_hi, u.s_lo, a.np / TB, pf ? std::atoi(pf) : 0};
-    const int split = u.split > 1 ? 2 : 1;
+    const int split = clamp_split(u.split);
     if (a.np % TB != 0 || grid % (2 * split) != 0 || (a.np / KC) % split != 0) return cudaErrorInvalidValue;
-    using K = void (*)(RelaxArgs, UmmaParams, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap);
-    K kern = split == 1 ? (u.jlo ? relax_dense_umma_kernel<true, 1> : relax_dense_umma_kernel<false, 1>)
-                        : (u.jlo ? relax_dense_umma_kernel<true, 2> : relax_dense_umma_kernel<false, 2>);
+    UmmaKernel kern = umma_kernel(split, u.jlo);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
     if (e != cudaSuccess) return e;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = SMEM_TOTAL;
-    cfg.stream = st;
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;        // split CTA pairs (cta_group::2)
-    attr[0].val.clusterDim.x = 2 * split;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cudaLaunchConfig_t cfg = umma_config(grid, split, st, attr);
     return cudaLaunchKernelEx(&cfg, kern, a, up, u.tm_shi, u.tm_slo, u.tm_jhi, u.tm_jlo);
 }
 

@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace marsb200 {
@@ -53,19 +54,50 @@ __device__ __forceinline__ bool mbar_try_wait(std::uint64_t* bar, std::uint32_t 
     return ok != 0;
 }
 
-// Wait until the phase with the given parity has completed.  A pipeline bug must not hang
-// the GPU: after 20 s of waiting the kernel traps (the launch then fails with an error).
-__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
-    if (mbar_try_wait(bar, parity)) return;
-    std::uint64_t t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    for (std::uint32_t spin = 1;; ++spin) {
-        if (mbar_try_wait(bar, parity)) return;
-        if ((spin & 1023u) == 0) {
+// Host-mapped record of the first timed-out wait (set per translation unit by its launcher;
+// readable by the host after the trap has torn the context down): {1, block, thread, smem
+// address, parity, %globaltimer}
+static __device__ unsigned long long* g_hang_log = nullptr;
+// wait limit (ns); MARS_HANG_S overrides it for the tcgen05 relaxation kernel
+static __device__ unsigned long long g_hang_ns = 120000000000ull;
+
+// A pipeline bug must not hang the GPU: a barrier wait longer than 120 s (profiler replays
+// are slow) reports the barrier and traps (the launch then fails with an error).
+
+static __device__ __noinline__ void mbar_hang(std::uint64_t* bar, std::uint32_t parity) {
+    if (unsigned long long* h = g_hang_log) {
+        if (atomicCAS(h, 0ull, 1ull) == 0ull) {
+            volatile unsigned long long* v = h;
             std::uint64_t t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            if (t - t0 > 120000000000ull) __trap();   // 120 s: hang detector (profiler replays are slow)
+            v[1] = blockIdx.x;
+            v[2] = threadIdx.x;
+            v[3] = smem_u32(bar);
+            v[4] = parity;
+            v[5] = t;
+            __threadfence_system();
         }
+    }
+    printf("mars: mbarrier wait timed out (block %d, thread %d, smem 0x%x, parity %u)\n", blockIdx.x, threadIdx.x,
+           smem_u32(bar), parity);
+    __trap();
+}
+
+__device__ __forceinline__ bool hang_check(std::uint64_t& t0, std::uint32_t spin) {
+    if ((spin & 1023u) != 0) return false;
+    std::uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t0 == 0) t0 = t;
+    return t - t0 > g_hang_ns;
+}
+
+// Wait until the phase with the given parity has completed.
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
+    if (mbar_try_wait(bar, parity)) return;
+    std::uint64_t t0 = 0;
+    for (std::uint32_t spin = 1;; ++spin) {
+        if (mbar_try_wait(bar, parity)) return;
+        if (hang_check(t0, spin)) mbar_hang(bar, parity);
     }
 }
 
@@ -374,10 +406,26 @@ __device__ __forceinline__ void st_cluster_u32(std::uint32_t cluster_addr, std::
     asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(cluster_addr), "r"(v) : "memory");
 }
 
+// monotonic shared-memory counters (cannot alias the way a parity wait on an mbarrier can
+// when the signalling side runs two phases ahead)
+__device__ __forceinline__ void red_add_release_cta(std::uint32_t* ctr, std::uint32_t v) {
+    asm volatile("red.release.cta.shared::cta.add.u32 [%0], %1;\n" ::"r"(smem_u32(ctr)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_release_cluster(std::uint32_t cluster_addr, std::uint32_t v) {
+    asm volatile("red.release.cluster.shared::cluster.add.u32 [%0], %1;\n" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ std::uint32_t ld_acquire_cluster(const std::uint32_t* ctr) {
+    std::uint32_t v;
+    asm volatile("ld.acquire.cluster.shared::cta.u32 %0, [%1];\n" : "=r"(v) : "r"(smem_u32(ctr)) : "memory");
+    return v;
+}
+
 // wait with cluster-scope acquire (data written by the peer CTA before its remote arrive)
 __device__ __forceinline__ void mbar_wait_cluster(std::uint64_t* bar, std::uint32_t parity) {
     std::uint32_t ok = 0;
-    do {
+    std::uint64_t t0 = 0;
+    for (std::uint32_t spin = 0;; ++spin) {
+        if (hang_check(t0, spin)) mbar_hang(bar, parity);
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
@@ -385,7 +433,8 @@ __device__ __forceinline__ void mbar_wait_cluster(std::uint64_t* bar, std::uint3
             : "=r"(ok)
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
-    } while (!ok);
+        if (ok) return;
+    }
 }
 
 __device__ __forceinline__ void tmem_alloc_pair(std::uint32_t* dst_smem, std::uint32_t ncols) {

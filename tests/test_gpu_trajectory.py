@@ -56,6 +56,7 @@ def _states(g, name, n):
     ("pm256", "dense_simt", None, None),    # CUDA-core blocked kernel
     ("sk2000", "dense_umma", None, None),
     ("sk2000", "dense_umma", None, "2"),
+    ("sk2000", "dense_umma", None, "4"),       # four pairs per tile (cluster of 8)
     ("sk2000", "dense_simt", None, None),
     ("sk16384", "dense_umma", None, None),  # N >= 8192: split over two pairs by default
 ])
@@ -165,7 +166,7 @@ def test_fp32_replay_fixture_is_consistent():
     assert len(r["status"]) == len(g["status"]) and np.array_equal(r["status"], g["status"])
 
 
-@pytest.mark.parametrize("split", ["1", "2"])
+@pytest.mark.parametrize("split", ["1", "2", "4"])
 def test_split_k_batches_match_reference(split, monkeypatch):
     """The split-K tcgen05 path (two CTA pairs per 256-run tile, partial fields through L2) on
     whole batches: cfg1's instance against the reference's full batch (best energy exact, >= 98%
@@ -183,3 +184,25 @@ def test_split_k_batches_match_reference(split, monkeypatch):
     same = np.all(rec.spins == unpack_spins(g["spins_packed"], w.n)[:256], axis=1)
     assert same.mean() >= fp32_floor_gate(256), same.mean()
     assert np.array_equal(rec.energy[same], g["energy"][:256][same])
+
+
+@pytest.mark.parametrize("runs", [4096, 1024])
+def test_split_k_large_batches_repeat_exactly(runs):
+    """Default split-K at N = 8192 (two CTA pairs per tile at 4096 runs -- four would not fit
+    the resident clusters -- four pairs at 1024): short-schedule batches, three times each.
+    Every run completes, and a run's record does not depend on which slot or tile ran it, so
+    the repeats are bit-identical.  (This is the configuration whose end-of-batch hand-off once
+    deadlocked: a pair whose K range misses a block no longer waits on it.)"""
+    n = 8192
+    p = mb.IsingProblem.dense(n, mb.gen_sk_gaussian(n, 3))
+    assert p.kernel() == "dense_umma"
+    prm = mb.MarsParams(t_min=0.0, t_max=3.0, t_step=1.0, c_step=1.0, d_min=1e-4,
+                        start_mode=mb.StartMode.UniformRandom)
+    recs = [mb.run_shard(p, mb.BatchSpec(prm, runs, 5, keep_spins=True), 0, runs) for _ in range(3)]
+    assert np.all(recs[0].status != int(mb.RunStatus.Diverged))
+    assert np.count_nonzero(recs[0].status == int(mb.RunStatus.Ok)) > runs // 2
+    for r in recs[1:]:
+        assert np.array_equal(r.status, recs[0].status)
+        assert np.array_equal(r.energy, recs[0].energy)
+        assert np.array_equal(r.descent_iters, recs[0].descent_iters)
+        assert np.array_equal(r.spins, recs[0].spins)
