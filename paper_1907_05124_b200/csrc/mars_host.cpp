@@ -832,14 +832,15 @@ int batch_alloc(mars_batch* b) {
             tm = relax_dense_umma_slots_per_cta();
             per_cta = static_cast<std::size_t>(2) * tm * p->np * sizeof(__half);   // S_hi + S_lo rows
             // Persistent CTAs (in pairs): when the fp16 J planes fit in L2, only as many CTAs as
-            // keep their state planes (re-read by every spin block's GEMM) in 85% of L2 beside
-            // J.  cfg2 (N = 2000, round 2 kernel) measured 11.5K descents/s at 148 CTAs, 12.6K
-            // at 110, 12.8K at 96 (this rule: 96).  MARS_UMMA_GRID overrides.
+            // keep their state planes (re-read by every spin block's GEMM) in 90% of L2 beside
+            // J.  cfg2 (N = 2000, round 2 kernel, power-capped): 11.5K descents/s at 148 CTAs,
+            // 12.6K at 110 (one box); 11.81K at 92, 12.0K at 98, 11.85K at 104 (another box,
+            // same call).  This rule: 98.  MARS_UMMA_GRID overrides.
             int l2 = 0;
             cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, p->device);
             const std::size_t jbytes = static_cast<std::size_t>(2) * p->np * p->np * sizeof(__half);
             int fit = p->num_sms;
-            const std::size_t l2use = static_cast<std::size_t>(l2) * 85 / 100;   // headroom: J32 diag, s0, spins
+            const std::size_t l2use = static_cast<std::size_t>(l2) * 90 / 100;   // headroom: J32 diag, s0, spins
             if (l2 > 0 && jbytes < l2use)
                 fit = static_cast<int>((l2use - jbytes) / per_cta);
             fit = std::max(p->num_sms / 2, std::min(p->num_sms, fit));

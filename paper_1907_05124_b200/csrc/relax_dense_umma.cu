@@ -108,6 +108,9 @@ struct __align__(8) Ctl {
     // monotonic count, not an mbarrier: with split-K a pair whose K range misses a block need
     // not wait for it, so the walkers may be any number of blocks past such a pair's producer.
     std::uint32_t wb[2];
+    std::uint64_t chunk_ready[2];   // SPLIT == 1: the same signal as an mbarrier (NW arrivals per
+                                    // half block; the producer reads every block, so its parity
+                                    // waits cannot alias) -- the hardware wake-up is faster
     volatile std::uint32_t stop;    // end of the batch (set by pair 0's walkers in every CTA)
     volatile std::uint32_t poison;  // 1 + the sequence number of the stage the leader producer
                                     // arrived on without data when it stopped (0 = running)
@@ -432,6 +435,10 @@ __device__ __forceinline__ bool pair_any(Ctl& ctl, bool local, bool lead, std::u
 template <int SPLIT>
 __device__ __forceinline__ void signal_writeback(Ctl& ctl, int hb, int half, int lane) {
     fence_proxy_async_global();
+    if constexpr (SPLIT == 1) {
+        mbar_arrive(&ctl.chunk_ready[hb]);
+        return;
+    }
     __syncwarp();
     if (lane == 0) {
         red_add_release_cta(&ctl.wb[hb], 1u);
@@ -439,8 +446,14 @@ __device__ __forceinline__ void signal_writeback(Ctl& ctl, int hb, int half, int
     }
 }
 
-// wait until the write-back counter of half `hb` reaches `target` (4 per block written back)
+// wait until half `hb` of block target/4 - 1 has been written back (the counter reaches
+// `target`, 4 per block; SPLIT == 1: that block's mbarrier phase)
+template <int SPLIT>
 __device__ __forceinline__ void wait_writeback(Ctl& ctl, int hb, std::uint32_t target) {
+    if constexpr (SPLIT == 1) {
+        mbar_wait(&ctl.chunk_ready[hb], (target / 4 - 1) & 1);
+        return;
+    }
     if (ld_acquire_cluster(&ctl.wb[hb]) >= target) return;
     std::uint64_t h0 = 0;
     for (std::uint32_t spin = 1; ld_acquire_cluster(&ctl.wb[hb]) < target; ++spin) {
@@ -484,6 +497,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
             mbar_init(&ctl.tmem_empty[s], 2 * NW);   // leader's: both CTAs' walkers
             mbar_init(&ctl.pair_more[s], 1);
             ctl.wb[s] = 0;
+            mbar_init(&ctl.chunk_ready[s], NW);
             mbar_init(&ctl.part_ready[s], NW * (SPLIT - 1) + (SPLIT == 1));
             mbar_init(&ctl.jready[s], NW);
         }
@@ -542,7 +556,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     const bool sweep_end = b == 0 && j == nk - CPB / 2;
                     if ((j == nk - CPB || j == nk - CPB / 2) && g > 0 && (mine || sweep_end)) {
                         const long long t0 = clock64();
-                        wait_writeback(ctl, j == nk - CPB ? 0 : 1, 4u * g);
+                        wait_writeback<SPLIT>(ctl, j == nk - CPB ? 0 : 1, 4u * g);
                         w_ready += clock64() - t0;
                         if (sweep_end && ctl.stop) {
                             // end of the batch: the next stage carries no data; the leader names
@@ -682,7 +696,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 tc_fence_after();
                 // xpart[buf] last held block g-2: pair 0 is done with it once its walkers are
                 // past that block (its helpers finish a block before its walkers do)
-                if (g >= 2) wait_writeback(ctl, 1, 4u * (g - 1));
+                if (g >= 2) wait_writeback<SPLIT>(ctl, 1, 4u * (g - 1));
                 float* dst = up.xpart + (((pair - 1) * 2 + buf) * plane + row0 + r) * static_cast<std::size_t>(TB);
 #pragma unroll 1
                 for (int cc = 0; cc < TB / 16; ++cc) {
