@@ -21,6 +21,7 @@
 #include <string>
 #include <thread>
 #include <utility>
+#include <queue>
 #include <vector>
 
 #include "../../include/mars_b200.h"
@@ -883,20 +884,56 @@ int batch_alloc(mars_batch* b) {
     int split = 1;
     if (p->kernel == MARS_KERNEL_DENSE_UMMA && !b->use_small) {
         b->grid = std::max(2, b->grid + (b->grid & 1));   // CTA pairs (cta_group::2)
-        // Split-K for large N: the field GEMM of a block (K = N) dwarfs its walk, and a batch
-        // of few 256-run tiles would leave most SMs idle -- two CTA pairs per tile, each taking
-        // half of K, when the doubled grid still fits (cfg5: 8192 runs -> 128 CTAs).
-        // MARS_UMMA_SPLIT=1/2/4 forces.
-        // Up to 4 pairs per tile (a cluster of 8) for small shards, e.g. the 1024-run share of
-        // an 8-GPU cfg5 run.
+        // Split-K for large N (np >= 8192): the field GEMM of a block (K = N) dwarfs its walk,
+        // so a 256-run tile's K range is split over 2 or 4 CTA pairs of one cluster, which
+        // makes each of its runs sweep faster (cfg5, cycles per block: 276K / 151K / 106K at
+        // split 1 / 2 / 4).  A batch lasts as long as its slowest slot, and runs are queued
+        // longest first (descending start temperature), so fewer but faster slots can win:
+        // pick the split and tile count minimising a greedy longest-first makespan estimate
+        // (work of a run ~ its level count).  cfg5 (8192 runs), measured: split 2 on 32 tiles
+        // (8192 slots) 11.2 descents/s; split 4 on 15 tiles (3840 slots) 17.9.  Every
+        // candidate keeps the whole grid one wave of resident clusters.
+        // MARS_UMMA_SPLIT=1/2/4 forces the split (tiles: as many as fit).
         const int se = env_int("MARS_UMMA_SPLIT", -1);
         const int nkc = p->np / relax_dense_umma_kc();
-        for (int cand : {4, 2})
-            if (split == 1 && (se == cand || (se < 0 && p->np >= 8192)) && cand * b->grid <= p->num_sms &&
-                nkc % cand == 0)
-                split = cand;
-        // the whole grid must be resident at once (one wave of clusters)
-        while (split > 1 && relax_dense_umma_max_clusters(split, p->jlo) < b->grid / 2) split /= 2;
+        const int pairs = b->grid / 2;                        // tiles the batch asks for
+        auto tiles_for = [&](int sp) {
+            const int resident = relax_dense_umma_max_clusters(sp, p->jlo);
+            return std::min({pairs, resident, p->num_sms / (2 * sp)});
+        };
+        if (se > 1 || (se < 0 && p->np >= 8192)) {
+            std::vector<double> work;                          // queue order (longest first)
+            work.reserve(static_cast<std::size_t>(b->queue_len));
+            for (int k = 0; k < b->queue_len; ++k) {
+                const double t0 = b->temp[static_cast<std::size_t>(b->h_order[k])];
+                work.push_back(std::floor(std::max(0.0, t0 - b->prm.t_min) / b->prm.t_step) + 1.0);
+            }
+            auto makespan = [&](int slots) {                   // greedy: next run -> earliest-free slot
+                std::priority_queue<double, std::vector<double>, std::greater<double>> q;
+                for (int i = 0; i < slots; ++i) q.push(0.0);
+                double end = 0.0;
+                for (double w : work) {
+                    const double t = q.top() + w;
+                    q.pop();
+                    q.push(t);
+                    end = std::max(end, t);
+                }
+                return end;
+            };
+            double best = -1.0;
+            for (int sp : {1, 2, 4}) {
+                if ((se > 1 && sp != se) || nkc % sp != 0) continue;
+                const int tl = tiles_for(sp);
+                if (tl < 1) continue;
+                static const double kSpeed[5] = {0.0, 1.0, 1.83, 0.0, 2.6};   // per-run sweep rate
+                const double est = makespan(tl * 2 * relax_dense_umma_slots_per_cta()) / kSpeed[sp];
+                if (best < 0.0 || est < best * 0.98) {          // prefer the smaller split on a near tie
+                    best = est;
+                    split = sp;
+                    b->grid = 2 * tl;
+                }
+            }
+        }
         if (std::getenv("MARS_UMMA_DEBUG"))
             std::fprintf(stderr, "[mars umma] pairs %d split %d resident clusters %d/%d/%d (split 1/2/4)\n", b->grid / 2,
                          split, relax_dense_umma_max_clusters(1, p->jlo), relax_dense_umma_max_clusters(2, p->jlo),
@@ -1467,6 +1504,27 @@ int execute_impl(mars_batch_t* b, mars_timing_t* timing, int fixed_sweeps, float
         ra.retire_head = d_head;
     }
     ra.state_out = d_state_out;
+    if (p->kernel == MARS_KERNEL_DENSE_UMMA && !b->use_small && std::getenv("MARS_L2_PERSIST")) {
+        // experiment: a persisting-L2 carve-out (evict_last lines) and an access-policy window
+        // over the state planes (MARS_L2_PERSIST=1: carve-out only, =2: + window)
+        int maxp = 0, maxw = 0;
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, p->device);
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, p->device);
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<std::size_t>(maxp));
+        if (std::atoi(std::getenv("MARS_L2_PERSIST")) >= 2) {
+            cudaStreamAttrValue v{};
+            v.accessPolicyWindow.base_ptr = b->d_work;
+            v.accessPolicyWindow.num_bytes = std::min<std::size_t>(b->work_bytes, static_cast<std::size_t>(maxw));
+            v.accessPolicyWindow.hitRatio =
+                std::min(1.0f, static_cast<float>(maxp) / static_cast<float>(v.accessPolicyWindow.num_bytes));
+            v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
+        }
+        if (std::getenv("MARS_UMMA_DEBUG"))
+            std::fprintf(stderr, "[mars umma] persisting L2 max %d B, window max %d B, state planes %zu B\n", maxp, maxw,
+                         b->work_bytes);
+    }
     std::int64_t launches = 0;
     const bool prof = std::getenv("MARS_PROFILE") != nullptr;
     long long* dprof = nullptr;

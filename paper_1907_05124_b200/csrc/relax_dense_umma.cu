@@ -152,6 +152,8 @@ struct UmmaParams {
     int nb;                  // blocks per sweep = np / TB
     int pf;                  // L2 prefetch distance of the state tiles, in chunks (0 = off; measured
                              // slower on cfg2 at 8 and 16 -- extra L2 pressure), MARS_UMMA_PF
+    int spol;                // L2 policy of the state-tile loads: 0 evict_normal, 1 evict_last,
+                             // 2 evict_first (MARS_UMMA_SPOL)
 };
 
 __device__ __forceinline__ void split16(float v, __half& hi, __half& lo, float& back) {
@@ -537,7 +539,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         }
         __syncwarp();
         const std::uint64_t jpol = policy_evict_last();
-        const std::uint64_t spol = policy_evict_normal();
+        const std::uint64_t spol = up.spol == 1 ? policy_evict_last() : up.spol == 2 ? policy_evict_first() : policy_evict_normal();
         const std::uint32_t smem0 = smem_u32(base);
         const std::uint32_t full0 = smem_u32(&ctl.full[0]);
         const std::uint32_t tx = 2 * (JLO ? STAGE_BYTES : STAGE_BYTES - TILE_J);   // both CTAs' bytes
@@ -1077,7 +1079,8 @@ cudaError_t launch_relax_dense_umma(const RelaxArgs& a, const UmmaLaunch& u, int
     unsigned long long* hang = nullptr;
     if (cudaError_t e = relax_dense_umma_hang_log(&hang)) return e;
     const char* pf = std::getenv("MARS_UMMA_PF");
-    UmmaParams up{u.xpart, u.s_hi, u.s_hi, u.s_lo, a.np / TB, pf ? std::atoi(pf) : 0};
+    const char* sp = std::getenv("MARS_UMMA_SPOL");
+    UmmaParams up{u.xpart, u.s_hi, u.s_hi, u.s_lo, a.np / TB, pf ? std::atoi(pf) : 0, sp ? std::atoi(sp) : 0};
     const int split = clamp_split(u.split);
     if (a.np % TB != 0 || grid % (2 * split) != 0 || (a.np / KC) % split != 0) return cudaErrorInvalidValue;
     UmmaKernel kern = umma_kernel(split, u.jlo);
