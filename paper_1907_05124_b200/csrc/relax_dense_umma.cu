@@ -153,7 +153,10 @@ struct UmmaParams {
     int pf;                  // L2 prefetch distance of the state tiles, in chunks (0 = off; measured
                              // slower on cfg2 at 8 and 16 -- extra L2 pressure), MARS_UMMA_PF
     int spol;                // L2 policy of the state-tile loads: 0 evict_normal, 1 evict_last,
-                             // 2 evict_first (MARS_UMMA_SPOL)
+                             // 2 evict_first (default: measured on cfg2, same box, 3 runs each:
+                             // 12.52K vs 12.17K descents/s, DRAM 11.8 vs 14.0 TB per launch,
+                             // L2 hit rate 55.6% vs 50.8%), MARS_UMMA_SPOL
+    int jpol;                // the same for the coupling tiles (default 1, evict_last), MARS_UMMA_JPOL
 };
 
 __device__ __forceinline__ void split16(float v, __half& hi, __half& lo, float& back) {
@@ -356,6 +359,95 @@ __device__ __forceinline__ void tmem_st16f(std::uint32_t taddr, const float (&v)
     tmem_st16(taddr, r);
 }
 
+// ---- helper rectangles on the warp-level tensor core (mma.sync.m16n8k16, fp16 hi/lo split,
+// fp32 accumulate).  A helper warp's 32 runs are two 16-run m-tiles (TMEM lanes 32q..+15,
+// 32q+16..+31).  tcgen05.ld/st .16x256b hand each thread exactly the mma fragment layout:
+// register e of a 16 x 8-column group is (lane g + 8*(e>>1), column 2c + (e&1)), g = lane/4,
+// c = lane%4 -- the f32 C/D fragment, and, packed in pairs, the f16 A fragment.  The coupling
+// fragments (8 fp32 values per 16 x 16 rectangle, from the diagonal triangle) are loaded per
+// thread with distinct addresses, instead of 64 warp-broadcast LDS.128 per rectangle.
+#ifndef MARS_HELPER_MMA
+#define MARS_HELPER_MMA 1
+#endif
+
+__device__ __forceinline__ void tmem_ld_16x256_x2(std::uint32_t taddr, float (&v)[8]) {
+    std::uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_st_16x256_x2(std::uint32_t taddr, const float (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.16x256b.x2.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr),
+                 "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                 "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+                 "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+                 : "memory");
+}
+
+__device__ __forceinline__ std::uint32_t h2_bits(__half2 h) { return *reinterpret_cast<std::uint32_t*>(&h); }
+
+// x0, x1 (x0 at the lower index) -> packed fp16 hi pair and lo pair (x = hi + lo)
+__device__ __forceinline__ void split_pair(float x0, float x1, std::uint32_t& hi, std::uint32_t& lo) {
+    const __half2 h = __floats2half2_rn(x0, x1);
+    const float2 hf = __half22float2(h);
+    hi = h2_bits(h);
+    lo = h2_bits(__floats2half2_rn(x0 - hf.x, x1 - hf.y));
+}
+
+__device__ __forceinline__ void mma_16816(float& c0, float& c1, float& c2, float& c3, const std::uint32_t (&a)[4],
+                                          std::uint32_t b0, std::uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};\n"
+                 : "+f"(c0), "+f"(c1), "+f"(c2), "+f"(c3)
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// fields f[m][8] (m-tile m: 16 runs x 16 columns of target sub-block t, prescaled units) +=
+// Delta_u (TMEM history, this warp's runs) x J[u rows][t columns] * jup, jup = 2^jexp (the
+// couplings in the same prescaled units, inside fp16's range)
+__device__ __forceinline__ void rect_mma(float (&f)[2][8], std::uint32_t tdel, const float* jtri, int u, int t,
+                                         float jup, int lane) {
+    const int g = lane >> 2, c = lane & 3;
+    // coupling fragments: B[k][n] = J[16u + k][16t + 8nt + n]; this thread: k = 2c, 2c+1, 2c+8, 2c+9, n = g
+    std::uint32_t bh[2][2], bl[2][2];
+    {
+        float jv[2][4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            const int i = 16 * u + 2 * c + (kk & 1) + 8 * (kk >> 1);
+            const float* row = jtri + tri_row_off_rt(i) - tri_k0(i) + 16 * t + g;
+            jv[0][kk] = row[0] * jup;
+            jv[1][kk] = row[8] * jup;
+        }
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            split_pair(jv[nt][0], jv[nt][1], bh[nt][0], bl[nt][0]);
+            split_pair(jv[nt][2], jv[nt][3], bh[nt][1], bl[nt][1]);
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+        float d[8];
+        tmem_ld_16x256_x2(tdel + (static_cast<std::uint32_t>(16 * m) << 16) + u * SB, d);
+        std::uint32_t ah[4], al[4];
+        split_pair(d[0], d[1], ah[0], al[0]);
+        split_pair(d[2], d[3], ah[1], al[1]);
+        split_pair(d[4], d[5], ah[2], al[2]);
+        split_pair(d[6], d[7], ah[3], al[3]);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            float* acc = &f[m][4 * nt];
+            mma_16816(acc[0], acc[1], acc[2], acc[3], ah, bh[nt][0], bh[nt][1]);
+            mma_16816(acc[0], acc[1], acc[2], acc[3], al, bh[nt][0], bh[nt][1]);
+            mma_16816(acc[0], acc[1], acc[2], acc[3], ah, bl[nt][0], bl[nt][1]);
+        }
+    }
+}
+
 struct Old16 {
     uint4 h[2], l[2];
 };
@@ -538,7 +630,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
             if (JLO) tma_prefetch_desc(&tm_jlo);
         }
         __syncwarp();
-        const std::uint64_t jpol = policy_evict_last();
+        const std::uint64_t jpol = up.jpol == 1 ? policy_evict_last() : up.jpol == 2 ? policy_evict_first() : policy_evict_normal();
         const std::uint64_t spol = up.spol == 1 ? policy_evict_last() : up.spol == 2 ? policy_evict_first() : policy_evict_normal();
         const std::uint32_t smem0 = smem_u32(base);
         const std::uint32_t full0 = smem_u32(&ctl.full[0]);
@@ -905,6 +997,8 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
         std::uint32_t g = 0, fe = 0, de = 0;
         long long c_dw = 0, c_work = 0, c_tw = 0, h_sweeps = 0;
         const std::size_t xplane = static_cast<std::size_t>(gridDim.x / (2 * SPLIT)) * 2 * TM;
+        const std::uint32_t tdel = tmem + lane_t + DEL_COL;   // this quarter's Delta history
+        const float jup = 1.0f / a.jscale;                    // 2^jexp (exact)
         issue_jtri(Jtri0, a.J32, np, 0, ht);
         cp_async_arrive_noinc(&ctl.jready[0]);
         for (;;) {
@@ -928,6 +1022,32 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     // else only while t < nsub) -- mirrors the walker's arrivals
                     const bool target = t < nsub;
                     if (!target && t - 2 > 0) break;
+#if MARS_HELPER_MMA
+                    float f[2][8];
+                    if (target) {
+#pragma unroll
+                        for (int m = 0; m < 2; ++m)
+                            tmem_ld_16x256_x2(tmem + (static_cast<std::uint32_t>(q * 32 + 16 * m) << 16) + buf * TB + t * SB, f[m]);
+                        if constexpr (SPLIT > 1) {
+                            const int gq = lane >> 2, cq = lane & 3;
+#pragma unroll
+                            for (int pp = 0; pp < SPLIT - 1; ++pp)
+#pragma unroll
+                                for (int m = 0; m < 2; ++m)
+#pragma unroll
+                                    for (int pr = 0; pr < 4; ++pr) {
+                                        const std::size_t row = row0 + q * 32 + 16 * m + gq + 8 * (pr & 1);
+                                        const int col = t * SB + 8 * (pr >> 1) + 2 * cq;
+                                        const float2 x = __ldcg(reinterpret_cast<const float2*>(
+                                            up.xpart + ((pp * 2 + buf) * xplane + row) * TB + col));
+                                        f[m][2 * pr] += x.x;
+                                        f[m][2 * pr + 1] += x.y;
+                                    }
+                        }
+                        // Deltas already final: sub-blocks 0 .. t-3
+                        for (int u = 0; u + 3 <= t; ++u) rect_mma(f, tdel, jtri, u, t, jup, lane);
+                    }
+#else
                     float2 pf[SB / 2];
                     if (target) {
                         float pv[SB];
@@ -942,6 +1062,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                             apply_rect16(pf, jtri, u * SB, t * SB, du);
                         }
                     }
+#endif
                     t0 = clock64();
                     c_work += t0 - t1;
                     mbar_wait(&ctl.dready[q][de & 1], (de >> 1) & 1);
@@ -957,6 +1078,15 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         staged = true;
                     }
                     if (!target) break;
+#if MARS_HELPER_MMA
+                    rect_mma(f, tdel, jtri, t - 2, t, jup, lane);
+#pragma unroll
+                    for (int m = 0; m < 2; ++m) {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) f[m][e] *= a.jscale;
+                        tmem_st_16x256_x2(tmem + (static_cast<std::uint32_t>(q * 32 + 16 * m) << 16) + buf * TB + t * SB, f[m]);
+                    }
+#else
                     float du[SB];
                     tmem_ld16(tmem + lane_t + DEL_COL + (t - 2) * SB, du);
                     apply_rect16(pf, jtri, (t - 2) * SB, t * SB, du);
@@ -967,6 +1097,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         pv[2 * j + 1] = pf[j].y;
                     }
                     tmem_st16f(tacc + t * SB, pv);
+#endif
                     tmem_st_wait();
                     tc_fence_before();
                     mbar_arrive(&ctl.fready[q][fe & 1]);
@@ -1080,7 +1211,9 @@ cudaError_t launch_relax_dense_umma(const RelaxArgs& a, const UmmaLaunch& u, int
     if (cudaError_t e = relax_dense_umma_hang_log(&hang)) return e;
     const char* pf = std::getenv("MARS_UMMA_PF");
     const char* sp = std::getenv("MARS_UMMA_SPOL");
-    UmmaParams up{u.xpart, u.s_hi, u.s_hi, u.s_lo, a.np / TB, pf ? std::atoi(pf) : 0, sp ? std::atoi(sp) : 0};
+    const char* jp = std::getenv("MARS_UMMA_JPOL");
+    UmmaParams up{u.xpart, u.s_hi, u.s_hi, u.s_lo, a.np / TB, pf ? std::atoi(pf) : 0, sp ? std::atoi(sp) : 2,
+                  jp ? std::atoi(jp) : 1};
     const int split = clamp_split(u.split);
     if (a.np % TB != 0 || grid % (2 * split) != 0 || (a.np / KC) % split != 0) return cudaErrorInvalidValue;
     UmmaKernel kern = umma_kernel(split, u.jlo);
