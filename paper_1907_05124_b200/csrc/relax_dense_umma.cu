@@ -70,7 +70,17 @@ constexpr int TB = 128;      // spins per Gauss-Seidel block = UMMA N
 // former 2 x 64 KB ring kept ~1 (measured: the MMA waited on TMA, not on SMEM or the pipe).
 constexpr int KC = 32;
 constexpr int CPB = TB / KC; // chunks per block
-constexpr int STAGES = 6;
+// The diagonal block's triangle (33 KB) is double buffered (the helpers stage block b+1's
+// during block b).  MARS_JTRI_BUFS=1 single-buffers it (staged once the walkers are past the
+// block, inside their wait for the next GEMM) and spends the 33 KB on two more operand
+// stages: measured 0.8% slower on cfg2 (same box) -- the MMA's wait for operand data did not
+// shrink, so the ring depth is not what limits the GEMM (the shared-memory port is: an N=128
+// SS-MMA reads 96 B/clk of operands per SM on top of 64 B/clk of TMA writes).
+#ifndef MARS_JTRI_BUFS
+#define MARS_JTRI_BUFS 2
+#endif
+constexpr int JBUFS = MARS_JTRI_BUFS;
+constexpr int STAGES = JBUFS == 1 ? 8 : 6;
 constexpr int NT = 320;      // 2 control warps + 4 walker warps + 4 helper warps
 constexpr int EPI_W = 2;     // first walker warp
 constexpr int EPI_H = 6;     // first helper warp
@@ -95,7 +105,8 @@ struct __align__(8) Ctl {
     std::uint64_t tmem_full[2];
     std::uint64_t tmem_empty[2];
     std::uint64_t part_ready[2];    // split-K: the other pairs' partial fields of a block in L2
-    std::uint64_t jready[2];        // diagonal triangle staged (per smem buffer)
+    std::uint64_t jready[2];        // diagonal triangle staged (per block parity)
+    std::uint64_t wdone;            // walkers past a block (JBUFS == 1: the triangle may go)
     std::uint64_t fready[4][2];     // helper -> walker: pre-corrected fields (per lane quarter)
     std::uint64_t dready[4][2];     // walker -> helper: a sub-block's Deltas in TMEM
     std::uint64_t mma_done;
@@ -128,7 +139,7 @@ __host__ __device__ constexpr int tri_row_off(int i) {
 constexpr std::uint32_t SMEM_STAGES = STAGES * STAGE_BYTES;
 constexpr std::uint32_t TRI = tri_row_off(TB);
 constexpr std::uint32_t SMEM_TRI = ((TRI * 4 + 127) / 128) * 128;
-constexpr std::uint32_t SMEM_TOTAL = SMEM_STAGES + 2 * SMEM_TRI + sizeof(Ctl);
+constexpr std::uint32_t SMEM_TOTAL = SMEM_STAGES + JBUFS * SMEM_TRI + sizeof(Ctl);
 static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
 
 __device__ __forceinline__ bool epi_any(bool v) {
@@ -177,6 +188,21 @@ __device__ __forceinline__ int tri_row_off_rt(int i) {
 // the spin's trial so their latency hides under the tanh.  Each spin's change Delta is kept
 // in a register (del[I]) -- the walker stores the sub-block's Deltas to TMEM for the helper.
 constexpr int SB = 16;
+
+// Who applies sub-block t-1's Deltas to sub-block t.  With the helper on mma.sync (default)
+// the helper does every rectangle, the last one after the walker's hand-off, and the walker
+// only walks (MARS_WALK_FOLD=0: its fold's broadcast loads were the largest shared-memory
+// consumer after the UMMA operands).  With the CUDA-core helper the walker folds t-1 into
+// its walk of t-1 (off the serial chain) and the helper starts at t = 2.
+#ifndef MARS_HELPER_MMA
+#define MARS_HELPER_MMA 1
+#endif
+#ifndef MARS_WALK_FOLD
+#define MARS_WALK_FOLD (MARS_HELPER_MMA ? 0 : 1)
+#endif
+static_assert(MARS_HELPER_MMA || MARS_WALK_FOLD, "the CUDA-core helper needs the walker's fold");
+constexpr bool kWalkFold = MARS_WALK_FOLD != 0;
+constexpr int HT0 = kWalkFold ? 2 : 1;   // first sub-block the helper prepares
 
 // The same for row i = k0 + I with k0 a multiple of 16 and I < 16 a compile-time constant:
 // with Q = k0 / 4, a = I / 4, r = I % 4 the closed form of tri_row_off(i) - tri_k0(i) is
@@ -260,14 +286,16 @@ __device__ __forceinline__ void sub_step(float2 (&p)[SB / 2], float2 (&an)[SB / 
         c.dmax = fmaxf(c.dmax, fabsf(delta));
         if constexpr (I + 1 < SB)
             sub_update<I>(p, jr, delta, std::make_integer_sequence<int, SB / 4 - ((I + 1) & ~3) / 4>{});
-        // this spin's coupling to the NEXT sub-block's fields, accumulated off the serial chain
-        // (fills the walk's idle issue slots; added to the next sub-block's fields before it walks)
-        const float4* jn = reinterpret_cast<const float4*>(c.tr.template row<I>(k0 + SB));
+        if constexpr (kWalkFold) {
+            // this spin's coupling to the NEXT sub-block's fields, accumulated off the serial
+            // chain (added to the next sub-block's fields before it walks)
+            const float4* jn = reinterpret_cast<const float4*>(c.tr.template row<I>(k0 + SB));
 #pragma unroll
-        for (int g = 0; g < SB / 4; ++g) {
-            const float4 jv = jn[g];
-            an[2 * g] = ffma2(make_float2(jv.x, jv.y), delta, an[2 * g]);
-            an[2 * g + 1] = ffma2(make_float2(jv.z, jv.w), delta, an[2 * g + 1]);
+            for (int g = 0; g < SB / 4; ++g) {
+                const float4 jv = jn[g];
+                an[2 * g] = ffma2(make_float2(jv.x, jv.y), delta, an[2 * g]);
+                an[2 * g + 1] = ffma2(make_float2(jv.z, jv.w), delta, an[2 * g + 1]);
+            }
         }
     } else {
         nv[I] = old[I];
@@ -366,10 +394,6 @@ __device__ __forceinline__ void tmem_st16f(std::uint32_t taddr, const float (&v)
 // c = lane%4 -- the f32 C/D fragment, and, packed in pairs, the f16 A fragment.  The coupling
 // fragments (8 fp32 values per 16 x 16 rectangle, from the diagonal triangle) are loaded per
 // thread with distinct addresses, instead of 64 warp-broadcast LDS.128 per rectangle.
-#ifndef MARS_HELPER_MMA
-#define MARS_HELPER_MMA 1
-#endif
-
 __device__ __forceinline__ void tmem_ld_16x256_x2(std::uint32_t taddr, float (&v)[8]) {
     std::uint32_t r[8];
     asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
@@ -570,7 +594,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
     unsigned char* base = smem_raw;   // SWIZZLE_128B tiles need 1024-byte alignment (checked)
     if (threadIdx.x == 0 && (smem_u32(smem_raw) & 1023u) != 0) __trap();
     float* Jtri0 = reinterpret_cast<float*>(base + SMEM_STAGES);
-    Ctl& ctl = *reinterpret_cast<Ctl*>(base + SMEM_STAGES + 2 * SMEM_TRI);
+    Ctl& ctl = *reinterpret_cast<Ctl*>(base + SMEM_STAGES + JBUFS * SMEM_TRI);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int np = a.np, n = a.n, nb = up.nb, nk = np / KC;
@@ -594,6 +618,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
             mbar_init(&ctl.chunk_ready[s], NW);
             mbar_init(&ctl.part_ready[s], NW * (SPLIT - 1) + (SPLIT == 1));
             mbar_init(&ctl.jready[s], NW);
+            if (s == 0) mbar_init(&ctl.wdone, NW);
         }
         for (int q = 0; q < 4; ++q)
             for (int s = 0; s < 2; ++s) {
@@ -840,7 +865,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 const int b0 = b * TB;
                 const int lim = min(TB, n - b0);
                 const int nsub = (lim + SB - 1) / SB;
-                const float* jtri = Jtri0 + (g & 1) * (SMEM_TRI / 4);
+                const float* jtri = Jtri0 + (JBUFS == 2 ? (g & 1) * (SMEM_TRI / 4) : 0);
                 const int buf = g & 1;
                 long long t0 = clock64();
                 if (!active && (mode == kLoading || mode == kDrain)) {
@@ -894,16 +919,16 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     if (t + 1 < nsub) fetch_old16(hi_row + b0 + k0 + SB, lo_row + b0 + k0 + SB, pre);
                     t1 = clock64();
                     c_apply += t1 - tpre;                       // the old-state load wait
-                    if (t >= 2) {
+                    if (t >= HT0) {
                         mbar_wait(&ctl.fready[q][fe & 1], (fe >> 1) & 1);
                         ++fe;
                         tc_fence_after();
                     }
                     float pv[SB];
                     tmem_ld16(tacc + k0, pv);
-                    if (t < 2) add_partials<SPLIT>(pv, up.xpart, xplane, buf, row0 + r, k0);
-                    // raw GEMM fields (t < 2) are on the prescaled couplings; the helper's are not
-                    const float sc = t >= 2 ? 1.0f : a.jscale;
+                    if (t < HT0) add_partials<SPLIT>(pv, up.xpart, xplane, buf, row0 + r, k0);
+                    // raw GEMM fields (t < HT0) are on the prescaled couplings; the helper's are not
+                    const float sc = t >= HT0 ? 1.0f : a.jscale;
                     float2 pf[SB / 2];
 #pragma unroll
                     for (int j = 0; j < SB / 2; ++j) {
@@ -920,8 +945,8 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     t0 = clock64();
                     c_walk += t0 - t1;
                     if (active) store_new16(hi_row + b0 + k0, lo_row + b0 + k0, nv);
-                    if (t == 0 || t + 2 < nsub) {
-                        // the helper needs this sub-block's Deltas (for sub-blocks >= t + 2)
+                    if (t == 0 || t + HT0 < nsub) {
+                        // the helper needs this sub-block's Deltas (for sub-blocks >= t + HT0)
                         tmem_st16f(tmem + lane_t + DEL_COL + k0, prev);
                         tmem_st_wait();
                         tc_fence_before();
@@ -935,6 +960,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     c_st += clock64() - t0;
                 }
                 dmax = fmaxf(dmax, ctx.dmax);
+                if (JBUFS == 1) mbar_arrive(&ctl.wdone);            // done with this block's triangle
                 tc_fence_before();
                 mbar_arrive_cluster(tmem_empty_leader + buf * 8);   // the leader's MMA reuses the buffer
                 if (b == nb - 1) {
@@ -1006,7 +1032,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 const int b0 = b * TB;
                 const int lim = min(TB, n - b0);
                 const int nsub = (lim + SB - 1) / SB;
-                const float* jtri = Jtri0 + (g & 1) * (SMEM_TRI / 4);
+                const float* jtri = Jtri0 + (JBUFS == 2 ? (g & 1) * (SMEM_TRI / 4) : 0);
                 const int buf = g & 1;
                 long long t0 = clock64();
                 mbar_wait(&ctl.jready[buf], (g >> 1) & 1);
@@ -1017,11 +1043,11 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 c_tw += t1 - t0;
                 const std::uint32_t tacc = tmem + lane_t + buf * TB;
                 bool staged = false;
-                for (int t = 2; t <= nsub + 1; ++t) {
-                    // target sub-block t (t < nsub); D-event for sub-block t-2 (t-2 = 0 always,
-                    // else only while t < nsub) -- mirrors the walker's arrivals
+                for (int t = HT0; t <= nsub + HT0 - 1; ++t) {
+                    // target sub-block t (t < nsub); D-event for sub-block t-HT0 (always for
+                    // sub-block 0, else only while t < nsub) -- mirrors the walker's arrivals
                     const bool target = t < nsub;
-                    if (!target && t - 2 > 0) break;
+                    if (!target && t - HT0 > 0) break;
 #if MARS_HELPER_MMA
                     float f[2][8];
                     if (target) {
@@ -1044,8 +1070,8 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                                         f[m][2 * pr + 1] += x.y;
                                     }
                         }
-                        // Deltas already final: sub-blocks 0 .. t-3
-                        for (int u = 0; u + 3 <= t; ++u) rect_mma(f, tdel, jtri, u, t, jup, lane);
+                        // Deltas already final: sub-blocks 0 .. t-HT0-1
+                        for (int u = 0; u + HT0 + 1 <= t; ++u) rect_mma(f, tdel, jtri, u, t, jup, lane);
                     }
 #else
                     float2 pf[SB / 2];
@@ -1070,7 +1096,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     tc_fence_after();
                     t1 = clock64();
                     c_dw += t1 - t0;
-                    if (t == 2 && !staged) {
+                    if (JBUFS == 2 && t == HT0 && !staged) {
                         // the walker is past the previous block: stage the next block's triangle
                         const int nb0 = (b + 1 == nb) ? 0 : b0 + TB;
                         issue_jtri(Jtri0 + ((g + 1) & 1) * (SMEM_TRI / 4), a.J32, np, nb0, ht);
@@ -1079,7 +1105,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     }
                     if (!target) break;
 #if MARS_HELPER_MMA
-                    rect_mma(f, tdel, jtri, t - 2, t, jup, lane);
+                    rect_mma(f, tdel, jtri, t - HT0, t, jup, lane);
 #pragma unroll
                     for (int m = 0; m < 2; ++m) {
 #pragma unroll
@@ -1105,6 +1131,13 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     t0 = clock64();
                     c_work += t0 - t1;
                     t1 = t0;
+                }
+                if (JBUFS == 1) {
+                    // the walkers are past this block: stage the next block's triangle over it
+                    mbar_wait(&ctl.wdone, g & 1);
+                    const int nb0 = (b + 1 == nb) ? 0 : b0 + TB;
+                    issue_jtri(Jtri0, a.J32, np, nb0, ht);
+                    cp_async_arrive_noinc(&ctl.jready[(g + 1) & 1]);
                 }
                 if (b == nb - 1) {
                     ++h_sweeps;

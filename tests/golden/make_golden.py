@@ -99,10 +99,10 @@ def cfg1():
     save("cfg1", **out)
 
 
-def prefix(name, runs, keep=None):
+def prefix(name, runs, keep=None, t_max=None, tag="_prefix"):
     w = WORKLOADS[name]
     p = build_oracle_problem(R, w)
-    pr = params(0, w.t_max, 1, 1, 1e-4, uniform=True)
+    pr = params(0, w.t_max if t_max is None else t_max, 1, 1, 1e-4, uniform=True)
     t = time.time()
     b = p.run_batch(pr, runs, w.base_seed, workers=0)
     print(f"{name} prefix {runs} runs {time.time() - t:.1f}s best {b.stats['best_energy']} "
@@ -110,7 +110,7 @@ def prefix(name, runs, keep=None):
     out = batch_arrays("", b, keep)
     out["coupling_sum"] = np.array([p.coupling_sum])
     out["wall_seconds"] = np.array([time.time() - t])
-    save(name + "_prefix", **out)
+    save(name + tag, **out)
 
 
 def small():
@@ -235,6 +235,10 @@ if __name__ == "__main__":
         replay_f32()
     if "cfg2" in which:
         prefix("cfg2_sk2000", 256)
+    if "cfg5" in which:
+        # cfg5's instance (N = 16384) on a short schedule (t_max = 3): the first 16 descents of
+        # the reference (~1 min per descent per core)
+        prefix("cfg5_sk16384", 16, t_max=3.0, tag="_t3_prefix")
     if "prefixes" in which:
         prefix("cfg2_sk2000", 256)
         prefix("cfg3a_er800", 256)

@@ -206,3 +206,25 @@ def test_split_k_large_batches_repeat_exactly(runs):
         assert np.array_equal(r.energy, recs[0].energy)
         assert np.array_equal(r.descent_iters, recs[0].descent_iters)
         assert np.array_equal(r.spins, recs[0].spins)
+
+
+def test_cfg5_short_prefix_against_reference():
+    """cfg5's instance (SK N = 16384) on a short schedule (t_max = 3): the first 16 descents
+    against the compiled reference's (tests/golden/cfg5_sk16384_t3_prefix.npz, made by
+    make_golden.py cfg5).  Through the default large-N path (split-K).  Same bars as the cfg2
+    prefix, with the spin agreement reported: status exact, energies bit-exact wherever the
+    rounded spins agree, the batch best equal or better, the mean within 0.5%."""
+    import dataclasses
+    g = golden("cfg5_sk16384_t3_prefix")
+    w = dataclasses.replace(WORKLOADS["cfg5_sk16384"], t_max=3.0)
+    p = build_problem(w)
+    rec = mb.run_shard(p, mb.BatchSpec(w.params(), 16, w.base_seed, keep_spins=True), 0, 16)
+    assert np.array_equal(rec.status, g["status"])
+    ok = rec.status == int(mb.RunStatus.Ok)
+    same = np.all(rec.spins == unpack_spins(g["spins_packed"], w.n), axis=1)
+    assert np.array_equal(rec.energy[same], g["energy"][same])
+    assert rec.energy[ok].min() <= g["energy"][ok].min() + 1e-9 * abs(g["energy"][ok].min())
+    assert abs(rec.energy[ok].mean() / g["energy"][ok].mean() - 1.0) < 5e-3
+    print(f"cfg5 t_max=3 prefix: {same.mean():.3f} of runs on the reference's spins; best {rec.energy[ok].min()} "
+          f"(reference {g['energy'][ok].min()}); mean iters {rec.descent_iters.mean():.1f} "
+          f"(reference {g['iters'].mean():.1f})")

@@ -1,0 +1,13 @@
+#!/bin/bash
+# single-buffered triangle + 8 stages (current) vs double-buffered + 6 stages (j2): parity, then same-box A/B
+mkdir -p gpurun_out/jb
+timeout 900 python -m pytest tests/test_gpu_trajectory.py tests/test_gpu_umma.py -x -q -k "not quench_consistency" > gpurun_out/jb/pytest.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/jb/pytest.log
+B="python bench.py --workload cfg2_sk2000 --steps 3 --warmup 3 --no-e2e --no-cpu"
+for rep in 1 2; do
+  for v in libmars_b200_j2.so libmars_b200.so; do
+    MARS_B200_LIB=$v timeout 300 $B >> gpurun_out/jb/cfg2_$v.json 2>> gpurun_out/jb/err.log
+  done
+done
+MARS_PROFILE=1 timeout 300 python bench.py --workload cfg2_sk2000 --steps 1 --warmup 1 --no-e2e --no-cpu --no-clocks > gpurun_out/jb/prof.json 2> gpurun_out/jb/prof.err
+echo done
