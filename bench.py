@@ -357,6 +357,14 @@ def run_b200(args, w, rank, world, local_rank, dist):
                 "kernel": f"relax_{kname}",
                 "peak_source": f"{src} bf16 sustained (MEASURED_PEAKS.json)",
                 "algorithmic": "2*N^2 flops per sweep-run x total sweeps per launch"}
+        if kname == "dense_umma":
+            # what the tensor cores actually execute: the fp32-accurate split issues 3 fp16
+            # products (2 for integer couplings) over the padded size np = ceil(N / 128) * 128
+            np_ = -(-w.n // 128) * 128
+            prods = 2 if w.kind == "sk_pm1" else 3
+            roof["executed"] = {"tflops": achieved_tf * prods * (np_ / w.n) ** 2,
+                                "frac": achieved_tf * prods * (np_ / w.n) ** 2 / bf16_sus,
+                                "model": f"{prods} fp16 UMMA products per coupling x (np/N)^2, np = {np_}"}
         if kname == "dense_small":
             roof["note"] = ("warp-per-run CUDA-core kernel for a batch resident at once: the time is the "
                             "longest descent's serial per-spin chain (div + tanhf + shuffle), so this "
