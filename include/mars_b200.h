@@ -207,6 +207,14 @@ int mars_debug_exchange(int32_t ranks, int64_t total, int32_t n, const uint8_t* 
                         double energy_tolerance, mars_records_t* records, mars_stats_t* stats,
                         int8_t* best_spins);
 
+/* TEST-ONLY: the tcgen05 kernel's large-N split-K choice (K1 "Split-K") on host
+ * data: runs with the given start temperatures, `pairs` CTA pairs asked for, the resident
+ * clusters of 2 / 4 / 8 CTAs, the SM count, the padded size np; forced = 2 or 4 forces the
+ * split (0: choose).  Returns the split (1, 2, 4) and the tile (CTA-pair) count. */
+int mars_debug_choose_split(const double* start_temps, int64_t count, const mars_params_t* prm, int32_t pairs,
+                            const int32_t resident[3], int32_t num_sms, int32_t np, int32_t forced,
+                            int32_t* split, int32_t* tiles);
+
 /* The reference's aggregation (runner.cpp:126-167) over `count` records in index order.
  * energy_tolerance: 0 for integral problems, 1e-9 otherwise (model.hpp:82). */
 int mars_aggregate(int64_t count, const uint8_t* status, const double* energy,

@@ -20,6 +20,7 @@ _MARS_NAMES = (
     "round_spins", "run_batch", "run_batch_with", "run_shard", "shard_range",
     "splitmix64", "sub_seed", "time_to_best", "validate", "debug_sweep",
     "NmfaParams", "SimCimParams", "run_batch_multi", "debug_exchange", "nmfa_defaults", "simcim_defaults", "linear_schedule", "schedule_at",
+    "debug_choose_split",
 )
 
 __all__ = list(_MARS_NAMES) + ["io", "mars", "workloads"]

@@ -103,6 +103,7 @@ SIGNATURES = {
     "mars_problem_replicate": (C.c_int, [vp, i32, C.POINTER(vp)]),
     "mars_run_batch_multi": (C.c_int, [vp, i32, P_params, i64, u64, vp, vp, vp]),
     "mars_debug_exchange": (C.c_int, [i32, i64, i32, vp, vp, vp, vp, vp, vp, dbl, vp, vp, vp]),
+    "mars_debug_choose_split": (C.c_int, [vp, i64, P_params, i32, vp, i32, i32, i32, vp, vp]),
     "mars_run_batch_nmfa": (C.c_int, [vp, C.POINTER(mars_nmfa_params_t), i64, u64, vp, vp, vp]),
     "mars_run_batch_simcim": (C.c_int, [vp, C.POINTER(mars_simcim_params_t), i64, u64, vp, vp, vp]),
     "mars_batch_fetch": (C.c_int, [vp, C.POINTER(mars_records_t), vp, vp]),

@@ -734,6 +734,51 @@ int sparse_config(mars_batch* b) {
     return MARS_OK;
 }
 
+// A run's expected work for the large-N schedule: its level count (the descent relaxes once
+// per temperature level from its start temperature down to t_min).
+double run_work(double t0, const mars_params_t& prm) {
+    return std::floor(std::max(0.0, t0 - prm.t_min) / prm.t_step) + 1.0;
+}
+
+// Greedy longest-first makespan of `work` (queue order) over `slots` identical slots.
+double greedy_makespan(const double* work, std::int64_t count, int slots) {
+    std::priority_queue<double, std::vector<double>, std::greater<double>> q;
+    for (int i = 0; i < slots; ++i) q.push(0.0);
+    double end = 0.0;
+    for (std::int64_t k = 0; k < count; ++k) {
+        const double t = q.top() + work[k];
+        q.pop();
+        q.push(t);
+        end = std::max(end, t);
+    }
+    return end;
+}
+
+// Split-K choice for np >= 8192 (K1 "Split-K"): among split 1 / 2 / 4 (or only
+// `forced`), the split and tile count (pairs) minimising greedy_makespan / per-run sweep rate,
+// a tile count limited by the pairs the batch asks for, the resident clusters of that split
+// and the SMs.  Rates from the measured cfg5 cycles per block (276K / 151K / 106K).  A near
+// tie (< 2%) keeps the smaller split.  Returns the split; *tiles_out the tile count.
+int choose_split(const double* work, std::int64_t count, int pairs, const int resident[3], int num_sms, int nkc,
+                 int forced, int slots_per_cta, int* tiles_out) {
+    static const double kSpeed[5] = {0.0, 1.0, 1.83, 0.0, 2.6};
+    int split = 1, tiles = std::max(1, std::min(pairs, num_sms / 2));
+    double best = -1.0;
+    for (int sp : {1, 2, 4}) {
+        if ((forced > 1 && sp != forced) || nkc % sp != 0) continue;
+        const int tl = std::min({pairs, resident[sp == 1 ? 0 : sp == 2 ? 1 : 2], num_sms / (2 * sp)});
+        if (tl < 1) continue;
+        const double est = greedy_makespan(work, count, tl * 2 * slots_per_cta) / kSpeed[sp];
+        if (best < 0.0 || est < best * 0.98) {
+            best = est;
+            split = sp;
+            tiles = tl;
+        }
+    }
+    *tiles_out = tiles;
+    return split;
+}
+
 int batch_alloc(mars_batch* b) {
     mars_problem* p = b->p;
     const std::size_t cnt = static_cast<std::size_t>(std::max<std::int64_t>(b->count, 1));
@@ -897,42 +942,17 @@ int batch_alloc(mars_batch* b) {
         const int se = env_int("MARS_UMMA_SPLIT", -1);
         const int nkc = p->np / relax_dense_umma_kc();
         const int pairs = b->grid / 2;                        // tiles the batch asks for
-        auto tiles_for = [&](int sp) {
-            const int resident = relax_dense_umma_max_clusters(sp, p->jlo);
-            return std::min({pairs, resident, p->num_sms / (2 * sp)});
-        };
         if (se > 1 || (se < 0 && p->np >= 8192)) {
             std::vector<double> work;                          // queue order (longest first)
             work.reserve(static_cast<std::size_t>(b->queue_len));
-            for (int k = 0; k < b->queue_len; ++k) {
-                const double t0 = b->temp[static_cast<std::size_t>(b->h_order[k])];
-                work.push_back(std::floor(std::max(0.0, t0 - b->prm.t_min) / b->prm.t_step) + 1.0);
-            }
-            auto makespan = [&](int slots) {                   // greedy: next run -> earliest-free slot
-                std::priority_queue<double, std::vector<double>, std::greater<double>> q;
-                for (int i = 0; i < slots; ++i) q.push(0.0);
-                double end = 0.0;
-                for (double w : work) {
-                    const double t = q.top() + w;
-                    q.pop();
-                    q.push(t);
-                    end = std::max(end, t);
-                }
-                return end;
-            };
-            double best = -1.0;
-            for (int sp : {1, 2, 4}) {
-                if ((se > 1 && sp != se) || nkc % sp != 0) continue;
-                const int tl = tiles_for(sp);
-                if (tl < 1) continue;
-                static const double kSpeed[5] = {0.0, 1.0, 1.83, 0.0, 2.6};   // per-run sweep rate
-                const double est = makespan(tl * 2 * relax_dense_umma_slots_per_cta()) / kSpeed[sp];
-                if (best < 0.0 || est < best * 0.98) {          // prefer the smaller split on a near tie
-                    best = est;
-                    split = sp;
-                    b->grid = 2 * tl;
-                }
-            }
+            for (int k = 0; k < b->queue_len; ++k)
+                work.push_back(run_work(b->temp[static_cast<std::size_t>(b->h_order[k])], b->prm));
+            const int resident[3] = {relax_dense_umma_max_clusters(1, p->jlo), relax_dense_umma_max_clusters(2, p->jlo),
+                                     relax_dense_umma_max_clusters(4, p->jlo)};
+            int tiles = 0;
+            split = choose_split(work.data(), static_cast<std::int64_t>(work.size()), pairs, resident, p->num_sms,
+                                 nkc, se > 1 ? se : 0, relax_dense_umma_slots_per_cta(), &tiles);
+            b->grid = 2 * tiles;
         }
         if (std::getenv("MARS_UMMA_DEBUG"))
             std::fprintf(stderr, "[mars umma] pairs %d split %d resident clusters %d/%d/%d (split 1/2/4)\n", b->grid / 2,
@@ -1013,6 +1033,22 @@ int plan_start_temps(const mars_params_t* prm, std::uint64_t base_seed, std::int
 extern "C" {
 
 const char* mars_last_error(void) { return g_err.c_str(); }
+
+int mars_debug_choose_split(const double* start_temps, int64_t count, const mars_params_t* prm, int32_t pairs,
+                            const int32_t resident[3], int32_t num_sms, int32_t np, int32_t forced, int32_t* split,
+                            int32_t* tiles) {
+    if (!start_temps || !prm || !resident || !split || !tiles || count < 0 || pairs < 1 || num_sms < 2 || np < 128)
+        return fail(MARS_ERR_INPUT, "mars_debug_choose_split: bad arguments");
+    std::vector<double> work(static_cast<std::size_t>(count));
+    for (int64_t k = 0; k < count; ++k) work[static_cast<std::size_t>(k)] = run_work(start_temps[k], *prm);
+    std::stable_sort(work.begin(), work.end(), std::greater<double>());   // the queue's longest-first order
+    const int res[3] = {resident[0], resident[1], resident[2]};
+    int t = 0;
+    *split = choose_split(work.data(), count, pairs, res, num_sms, np / relax_dense_umma_kc(), forced,
+                          relax_dense_umma_slots_per_cta(), &t);
+    *tiles = t;
+    return MARS_OK;
+}
 
 int mars_device_count(int* out) {
     CUDA_TRY(cudaGetDeviceCount(out));

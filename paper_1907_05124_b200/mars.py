@@ -684,6 +684,17 @@ def debug_exchange(ranks: int, records: Records, tolerance: float):
     return out, st, best
 
 
+def debug_choose_split(start_temps, params: MarsParams, pairs: int, resident=(74, 33, 15), num_sms: int = 148,
+                       np_: int = 16384, forced: int = 0):
+    """TEST-ONLY: the tcgen05 kernel's large-N split-K choice on host data -> (split, tiles)."""
+    t = np.ascontiguousarray(start_temps, np.float64)
+    res = np.ascontiguousarray(resident, np.int32)
+    sp, tl = C.c_int32(0), C.c_int32(0)
+    _check(lib.mars_debug_choose_split(ptr(t), len(t), C.byref(params._c()), int(pairs), ptr(res), int(num_sms),
+                                       int(np_), int(forced), C.byref(sp), C.byref(tl)))
+    return sp.value, tl.value
+
+
 def _replay_progress(stats: "BatchStats", progress: ProgressFn) -> None:
     best_so_far = float("inf")
     for k in range(len(stats.records.status)):
