@@ -76,6 +76,10 @@ constexpr int CPB = TB / KC; // chunks per block
 // stages: measured 0.8% slower on cfg2 (same box) -- the MMA's wait for operand data did not
 // shrink, so the ring depth is not what limits the GEMM (the shared-memory port is: an N=128
 // SS-MMA reads 96 B/clk of operands per SM on top of 64 B/clk of TMA writes).
+// Issue order of the three split products per K step (A/B experiment; 0: hi*hi, lo*hi, hi*lo)
+#ifndef MARS_UMMA_ORDER_A
+#define MARS_UMMA_ORDER_A 0
+#endif
 #ifndef MARS_JTRI_BUFS
 #define MARS_JTRI_BUFS 2
 #endif
@@ -770,12 +774,22 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         const std::uint64_t ahi = desc_k_sw64(st + kk * 32);
                         const std::uint64_t alo = desc_k_sw64(st + TILE_A + kk * 32);
                         const std::uint64_t jhi = desc_k_sw64(st + 2 * TILE_A + kk * 32);
+#if MARS_UMMA_ORDER_A
+                        // the two products sharing A_hi back to back
+                        mma_f16_ss_pair_elect(d, ahi, jhi, idesc, (cnt | kk) != 0);
+                        if (JLO) {
+                            const std::uint64_t jlo = desc_k_sw64(st + 2 * TILE_A + TILE_J + kk * 32);
+                            mma_f16_ss_pair_elect(d, ahi, jlo, idesc, 1);
+                        }
+                        mma_f16_ss_pair_elect(d, alo, jhi, idesc, 1);
+#else
                         mma_f16_ss_pair_elect(d, ahi, jhi, idesc, (cnt | kk) != 0);
                         mma_f16_ss_pair_elect(d, alo, jhi, idesc, 1);
                         if (JLO) {
                             const std::uint64_t jlo = desc_k_sw64(st + 2 * TILE_A + TILE_J + kk * 32);
                             mma_f16_ss_pair_elect(d, ahi, jlo, idesc, 1);
                         }
+#endif
                     }
                     mma_commit_pair_mc_elect(&ctl.empty[s], pair);
                     ++cnt;
