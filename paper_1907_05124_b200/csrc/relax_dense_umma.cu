@@ -76,7 +76,12 @@ constexpr int CPB = TB / KC; // chunks per block
 // stages: measured 0.8% slower on cfg2 (same box) -- the MMA's wait for operand data did not
 // shrink, so the ring depth is not what limits the GEMM (the shared-memory port is: an N=128
 // SS-MMA reads 96 B/clk of operands per SM on top of 64 B/clk of TMA writes).
-// Issue order of the three split products per K step (A/B experiment; 0: hi*hi, lo*hi, hi*lo)
+// All of a stage's MMAs under one elect (1) or one elect per MMA (0)
+#ifndef MARS_UMMA_STAGE_ISSUE
+#define MARS_UMMA_STAGE_ISSUE 1
+#endif
+// Issue order of the three split products per K step (A/B experiment; 0: hi*hi, lo*hi, hi*lo;
+// measured no difference)
 #ifndef MARS_UMMA_ORDER_A
 #define MARS_UMMA_ORDER_A 0
 #endif
@@ -769,6 +774,11 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     }
                     tc_fence_after();
                     const std::uint32_t st = smem0 + s * STAGE_BYTES;
+#if MARS_UMMA_STAGE_ISSUE
+                    static_assert(KC == 32, "one stage = two K steps of 16");
+                    mma_stage_split_pair_elect<JLO>(d, desc_k_sw64(st), desc_k_sw64(st + TILE_A), desc_k_sw64(st + 2 * TILE_A),
+                                                    desc_k_sw64(st + 2 * TILE_A + TILE_J), idesc, cnt != 0);
+#else
 #pragma unroll
                     for (int kk = 0; kk < KC / 16; ++kk) {
                         const std::uint64_t ahi = desc_k_sw64(st + kk * 32);
@@ -791,6 +801,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         }
 #endif
                     }
+#endif
                     mma_commit_pair_mc_elect(&ctl.empty[s], pair);
                     ++cnt;
                     ++seq;

@@ -459,6 +459,52 @@ __device__ __forceinline__ void mma_f16_ss_pair_elect(std::uint32_t d_tmem, std:
         : "memory");
 }
 
+// One operand stage of the fp32-accurate split on a CTA pair: for two K steps of 16 (the
+// descriptors of the second are the first's + 32 bytes, i.e. +2 in the address field),
+// A_hi*J_hi (accumulating unless `accumulate` is 0 on the first), A_lo*J_hi and, with JLO,
+// A_hi*J_lo -- all issued by one elected lane under one elect (the per-MMA elect / uniform-
+// register broadcast sequence was ~18 instructions per MMA).
+template <bool JLO>
+__device__ __forceinline__ void mma_stage_split_pair_elect(std::uint32_t d_tmem, std::uint64_t ahi, std::uint64_t alo,
+                                                           std::uint64_t jhi, std::uint64_t jlo, std::uint32_t idesc,
+                                                           std::uint32_t accumulate) {
+    if constexpr (JLO) {
+        asm volatile(
+            "{\n\t.reg .pred p, q, t;\n\t.reg .b64 a1, l1, h1, g1;\n\t"
+            "setp.ne.b32 q, %6, 0;\n\t"
+            "setp.eq.b32 t, 0, 0;\n\t"
+            "add.s64 a1, %1, 2;\n\t"
+            "add.s64 l1, %2, 2;\n\t"
+            "add.s64 h1, %3, 2;\n\t"
+            "add.s64 g1, %4, 2;\n\t"
+            "elect.sync _|p, 0xffffffff;\n\t"
+            "@p tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %3, %5, q;\n\t"
+            "@p tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %5, t;\n\t"
+            "@p tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %4, %5, t;\n\t"
+            "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a1, h1, %5, t;\n\t"
+            "@p tcgen05.mma.cta_group::2.kind::f16 [%0], l1, h1, %5, t;\n\t"
+            "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a1, g1, %5, t;\n\t}\n" ::"r"(d_tmem),
+            "l"(ahi), "l"(alo), "l"(jhi), "l"(jlo), "r"(idesc), "r"(accumulate)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p, q, t;\n\t.reg .b64 a1, l1, h1;\n\t"
+            "setp.ne.b32 q, %5, 0;\n\t"
+            "setp.eq.b32 t, 0, 0;\n\t"
+            "add.s64 a1, %1, 2;\n\t"
+            "add.s64 l1, %2, 2;\n\t"
+            "add.s64 h1, %3, 2;\n\t"
+            "elect.sync _|p, 0xffffffff;\n\t"
+            "@p tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %3, %4, q;\n\t"
+            "@p tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %4, t;\n\t"
+            "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a1, h1, %4, t;\n\t"
+            "@p tcgen05.mma.cta_group::2.kind::f16 [%0], l1, h1, %4, t;\n\t}\n" ::"r"(d_tmem),
+            "l"(ahi), "l"(alo), "l"(jhi), "r"(idesc), "r"(accumulate)
+            : "memory");
+        (void)jlo;
+    }
+}
+
 // commit the pair's MMAs to the barrier at the same offset in both CTAs of pair `pair` of the
 // cluster (ranks 2*pair, 2*pair + 1)
 __device__ __forceinline__ void mma_commit_pair_mc_elect(std::uint64_t* bar, int pair = 0) {
