@@ -51,6 +51,7 @@
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <utility>
 
 #include "kernels.cuh"
@@ -1235,13 +1236,16 @@ int relax_dense_umma_max_clusters(int split, bool jlo) {
 }
 
 // The host-mapped hang record (umma.cuh) of this translation unit's kernels, allocated once
-// per process; *host receives the host view.
+// per process and pointed to from each device's symbol on first use there; *host receives the
+// host view.  Thread-safe: the multi-GPU driver launches from one host thread per device.
 cudaError_t relax_dense_umma_hang_log(unsigned long long** host) {
+    static std::mutex mu;
     static unsigned long long* h = nullptr;
-    static int dev_set = -1;
+    static std::uint64_t devs_set = 0;   // bit d: device d's symbol points at h
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
     if (!h) {
         if ((e = cudaHostAlloc(reinterpret_cast<void**>(&h), 8 * sizeof(unsigned long long),
                                cudaHostAllocMapped | cudaHostAllocPortable)) != cudaSuccess) {
@@ -1250,7 +1254,7 @@ cudaError_t relax_dense_umma_hang_log(unsigned long long** host) {
         }
         for (int i = 0; i < 8; ++i) h[i] = 0;
     }
-    if (dev_set != dev) {
+    if (dev < 64 && !(devs_set >> dev & 1u)) {
         unsigned long long* d = nullptr;
         if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), h, 0)) != cudaSuccess) return e;
         if ((e = cudaMemcpyToSymbol(g_hang_log, &d, sizeof(d))) != cudaSuccess) return e;
@@ -1258,7 +1262,7 @@ cudaError_t relax_dense_umma_hang_log(unsigned long long** host) {
             const unsigned long long ns = static_cast<unsigned long long>(std::atof(hs) * 1e9);
             if ((e = cudaMemcpyToSymbol(g_hang_ns, &ns, sizeof(ns))) != cudaSuccess) return e;
         }
-        dev_set = dev;
+        devs_set |= std::uint64_t(1) << dev;
     }
     *host = h;
     return cudaSuccess;
