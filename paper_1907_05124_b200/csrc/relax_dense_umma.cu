@@ -178,6 +178,8 @@ struct UmmaParams {
                              // 12.52K vs 12.17K descents/s, DRAM 11.8 vs 14.0 TB per launch,
                              // L2 hit rate 55.6% vs 50.8%), MARS_UMMA_SPOL
     int jpol;                // the same for the coupling tiles (default 1, evict_last), MARS_UMMA_JPOL
+    int nowb;                // TIMING EXPERIMENT ONLY (wrong results): the producers do not wait for
+                             // the walkers' write-back except at the sweep boundary, MARS_UMMA_NOWB
 };
 
 __device__ __forceinline__ void split16(float v, __half& hi, __half& lo, float& back) {
@@ -683,7 +685,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     // raise `stop` before that write-back, so both producers of a pair stop at
                     // this same point of their stage sequence.
                     const bool sweep_end = b == 0 && j == nk - CPB / 2;
-                    if ((j == nk - CPB || j == nk - CPB / 2) && g > 0 && (mine || sweep_end)) {
+                    if ((j == nk - CPB || j == nk - CPB / 2) && g > 0 && (mine || sweep_end) && (!up.nowb || sweep_end)) {
                         const long long t0 = clock64();
                         wait_writeback<SPLIT>(ctl, j == nk - CPB ? 0 : 1, 4u * g);
                         w_ready += clock64() - t0;
@@ -1274,8 +1276,9 @@ cudaError_t launch_relax_dense_umma(const RelaxArgs& a, const UmmaLaunch& u, int
     const char* pf = std::getenv("MARS_UMMA_PF");
     const char* sp = std::getenv("MARS_UMMA_SPOL");
     const char* jp = std::getenv("MARS_UMMA_JPOL");
+    const char* nw = std::getenv("MARS_UMMA_NOWB");
     UmmaParams up{u.xpart, u.s_hi, u.s_hi, u.s_lo, a.np / TB, pf ? std::atoi(pf) : 0, sp ? std::atoi(sp) : 2,
-                  jp ? std::atoi(jp) : 1};
+                  jp ? std::atoi(jp) : 1, nw ? std::atoi(nw) : 0};
     const int split = clamp_split(u.split);
     if (a.np % TB != 0 || grid % (2 * split) != 0 || (a.np / KC) % split != 0) return cudaErrorInvalidValue;
     UmmaKernel kern = umma_kernel(split, u.jlo);
