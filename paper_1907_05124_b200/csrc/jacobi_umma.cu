@@ -386,6 +386,7 @@ cudaError_t launch_rng_probe(const std::uint64_t* seeds, int streams, int count,
 }
 
 int jacobi_umma_slots_per_cta() { return TM; }
+int jacobi_umma_kc() { return KC; }   // its operand maps' box width (independent of the relaxation kernel's)
 
 cudaError_t launch_jacobi_umma(const JacobiArgs& a, const JacobiLaunch& l, int grid, cudaStream_t st) {
     if (a.np % TB != 0 || grid % 2 != 0) return cudaErrorInvalidValue;

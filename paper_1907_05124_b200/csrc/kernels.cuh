@@ -144,6 +144,7 @@ constexpr int kMtWords = 312;   // mt19937_64 state words per run slot (mt_devic
 cudaError_t launch_rng_probe(const std::uint64_t* seeds, int streams, int count, std::uint64_t* st,
                              std::uint64_t* u64, double* gauss, cudaStream_t s);
 int jacobi_umma_slots_per_cta();
+int jacobi_umma_kc();            // K per stage of the Jacobi kernel (the TMA box width of its maps)
 
 // Level-scheduled sparse kernel (relax_csr.cu).  Spins grouped by Gauss-Seidel level,
 // levels cut into cw-spin chunks, each chunk's neighbour lists interleaved [k][cw].

@@ -159,7 +159,8 @@ struct mars_problem {
     bool jlo = true;                // J_lo nonzero somewhere (non-integer couplings)
     int jexp = 0;                   // power-of-two prescale of the fp16 planes
     int np16 = 0;                   // padded size of the fp16 planes (multiple of 128)
-    CUtensorMap tm_jhi{}, tm_jlo{};
+    CUtensorMap tm_jhi{}, tm_jlo{};          // relaxation kernel's boxes (relax_dense_umma_kc() wide)
+    CUtensorMap tm_jhi_j{}, tm_jlo_j{};      // the Jacobi kernel's (jacobi_umma_kc() wide)
     float* dNorm = nullptr;         // NMFA normalisers (lazily, fp32 [np16])
     // Buffer pool for the batches run on this problem: repeated run_batch calls reuse their
     // pinned host and device allocations (a 65536 x 2000 fp64 plan is 1 GB pinned) instead of
@@ -485,7 +486,9 @@ int build_umma_planes(mars_problem* p) {
     if (int rc = upload(&p->dJhi, jh.data(), jh.size())) return rc;
     if (int rc = upload(&p->dJlo, jl.data(), jl.size())) return rc;
     if (!make_tmap_f16(&p->tm_jhi, p->dJhi, np, np, relax_dense_umma_kc(), relax_dense_umma_j_rows()) ||
-        !make_tmap_f16(&p->tm_jlo, p->dJlo, np, np, relax_dense_umma_kc(), relax_dense_umma_j_rows()))
+        !make_tmap_f16(&p->tm_jlo, p->dJlo, np, np, relax_dense_umma_kc(), relax_dense_umma_j_rows()) ||
+        !make_tmap_f16(&p->tm_jhi_j, p->dJhi, np, np, jacobi_umma_kc(), relax_dense_umma_j_rows()) ||
+        !make_tmap_f16(&p->tm_jlo_j, p->dJlo, np, np, jacobi_umma_kc(), relax_dense_umma_j_rows()))
         return fail(MARS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the coupling planes");
     return MARS_OK;
 }
@@ -2030,10 +2033,10 @@ int run_jacobi(mars_problem* p, int solver, std::int64_t iters, const double* sc
     JacobiLaunch l{};
     for (int bsel = 0; bsel < 2; ++bsel)
         for (int pl = 0; pl < 2; ++pl)
-            if (!make_tmap_f16(&l.tm_s[bsel][pl], planes[2 * bsel + pl], slots, np, relax_dense_umma_kc(), tm))
+            if (!make_tmap_f16(&l.tm_s[bsel][pl], planes[2 * bsel + pl], slots, np, jacobi_umma_kc(), tm))
                 return fail(MARS_ERR_CUDA, "cuTensorMapEncodeTiled failed for the state planes");
-    l.tm_jhi = p->tm_jhi;
-    l.tm_jlo = p->tm_jlo;
+    l.tm_jhi = p->tm_jhi_j;
+    l.tm_jlo = p->tm_jlo_j;
     l.jlo = p->jlo;
     CUDA_TRY(launch_jacobi_umma(a, l, grid, st));
     EnergyArgs ea{n, p->dJ64, p->dOff, p->dIdx, p->dW64, p->dH64, p->coupling_sum,

@@ -69,7 +69,10 @@ constexpr int TB = 128;      // spins per Gauss-Seidel block = UMMA N
 // the operand stream (state + coupling tiles from L2/HBM) is latency bound, so what sets the
 // GEMM rate is the bytes in flight -- 5 x 32 KB stages keep ~4 loads outstanding where the
 // former 2 x 64 KB ring kept ~1 (measured: the MMA waited on TMA, not on SMEM or the pipe).
-constexpr int KC = 32;
+#ifndef MARS_UMMA_KC
+#define MARS_UMMA_KC 64
+#endif
+constexpr int KC = MARS_UMMA_KC;   // 32: SWIZZLE_64B rows; 64: SWIZZLE_128B rows (A/B variant)
 constexpr int CPB = TB / KC; // chunks per block
 // The diagonal block's triangle (33 KB) is double buffered (the helpers stage block b+1's
 // during block b).  MARS_JTRI_BUFS=1 single-buffers it (staged once the walkers are past the
@@ -79,7 +82,7 @@ constexpr int CPB = TB / KC; // chunks per block
 // SS-MMA reads 96 B/clk of operands per SM on top of 64 B/clk of TMA writes).
 // All of a stage's MMAs under one elect (1) or one elect per MMA (0)
 #ifndef MARS_UMMA_STAGE_ISSUE
-#define MARS_UMMA_STAGE_ISSUE 1
+#define MARS_UMMA_STAGE_ISSUE (MARS_UMMA_KC == 32)
 #endif
 // Issue order of the three split products per K step (A/B experiment; 0: hi*hi, lo*hi, hi*lo;
 // measured no difference)
@@ -90,7 +93,7 @@ constexpr int CPB = TB / KC; // chunks per block
 #define MARS_JTRI_BUFS 2
 #endif
 constexpr int JBUFS = MARS_JTRI_BUFS;
-constexpr int STAGES = JBUFS == 1 ? 8 : 6;
+constexpr int STAGES = (JBUFS == 1 ? 8 : 6) * 32 / KC;
 constexpr int NT = 320;      // 2 control warps + 4 walker warps + 4 helper warps
 constexpr int EPI_W = 2;     // first walker warp
 constexpr int EPI_H = 6;     // first helper warp
@@ -165,6 +168,15 @@ __device__ __forceinline__ bool epi_any(bool v) {
     return r != 0;
 }
 
+// K-major operand descriptor of this kernel's stage layout (64- or 128-byte swizzled rows)
+__device__ __forceinline__ std::uint64_t desc_k(std::uint32_t smem_addr) {
+    if constexpr (KC == 64) {
+        return desc_k_sw128(smem_addr);
+    } else {
+        return desc_k_sw64(smem_addr);
+    }
+}
+
 struct UmmaParams {
     float* xpart;            // split-K: partial fields of pairs 1.. [split-1][2][tile rows][TB] fp32
     const __half* s_hi;      // state planes (generic pointers for the epilogue)
@@ -180,6 +192,10 @@ struct UmmaParams {
     int jpol;                // the same for the coupling tiles (default 1, evict_last), MARS_UMMA_JPOL
     int nowb;                // TIMING EXPERIMENT ONLY (wrong results): the producers do not wait for
                              // the walkers' write-back except at the sweep boundary, MARS_UMMA_NOWB
+    int nohelp;              // TIMING EXPERIMENT ONLY (wrong results): the helpers skip their
+                             // rectangles (mma.sync), MARS_UMMA_NOHELP
+    int gemmonly;            // TIMING EXPERIMENT ONLY (wrong results; with MARS_UMMA_NOWB=1): walkers
+                             // and helpers skip the block's epilogue entirely, MARS_UMMA_GEMMONLY
 };
 
 __device__ __forceinline__ void split16(float v, __half& hi, __half& lo, float& back) {
@@ -207,7 +223,7 @@ constexpr int SB = 16;
 // consumer after the UMMA operands).  With the CUDA-core helper the walker folds t-1 into
 // its walk of t-1 (off the serial chain) and the helper starts at t = 2.
 #ifndef MARS_HELPER_MMA
-#define MARS_HELPER_MMA 1
+#define MARS_HELPER_MMA 0
 #endif
 #ifndef MARS_WALK_FOLD
 #define MARS_WALK_FOLD (MARS_HELPER_MMA ? 0 : 1)
@@ -778,20 +794,20 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     tc_fence_after();
                     const std::uint32_t st = smem0 + s * STAGE_BYTES;
 #if MARS_UMMA_STAGE_ISSUE
-                    static_assert(KC == 32, "one stage = two K steps of 16");
-                    mma_stage_split_pair_elect<JLO>(d, desc_k_sw64(st), desc_k_sw64(st + TILE_A), desc_k_sw64(st + 2 * TILE_A),
-                                                    desc_k_sw64(st + 2 * TILE_A + TILE_J), idesc, cnt != 0);
+                    static_assert(KC == 32 || !MARS_UMMA_STAGE_ISSUE, "one stage = two K steps of 16");
+                    mma_stage_split_pair_elect<JLO>(d, desc_k(st), desc_k(st + TILE_A), desc_k(st + 2 * TILE_A),
+                                                    desc_k(st + 2 * TILE_A + TILE_J), idesc, cnt != 0);
 #else
 #pragma unroll
                     for (int kk = 0; kk < KC / 16; ++kk) {
-                        const std::uint64_t ahi = desc_k_sw64(st + kk * 32);
-                        const std::uint64_t alo = desc_k_sw64(st + TILE_A + kk * 32);
-                        const std::uint64_t jhi = desc_k_sw64(st + 2 * TILE_A + kk * 32);
+                        const std::uint64_t ahi = desc_k(st + kk * 32);
+                        const std::uint64_t alo = desc_k(st + TILE_A + kk * 32);
+                        const std::uint64_t jhi = desc_k(st + 2 * TILE_A + kk * 32);
 #if MARS_UMMA_ORDER_A
                         // the two products sharing A_hi back to back
                         mma_f16_ss_pair_elect(d, ahi, jhi, idesc, (cnt | kk) != 0);
                         if (JLO) {
-                            const std::uint64_t jlo = desc_k_sw64(st + 2 * TILE_A + TILE_J + kk * 32);
+                            const std::uint64_t jlo = desc_k(st + 2 * TILE_A + TILE_J + kk * 32);
                             mma_f16_ss_pair_elect(d, ahi, jlo, idesc, 1);
                         }
                         mma_f16_ss_pair_elect(d, alo, jhi, idesc, 1);
@@ -799,7 +815,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                         mma_f16_ss_pair_elect(d, ahi, jhi, idesc, (cnt | kk) != 0);
                         mma_f16_ss_pair_elect(d, alo, jhi, idesc, 1);
                         if (JLO) {
-                            const std::uint64_t jlo = desc_k_sw64(st + 2 * TILE_A + TILE_J + kk * 32);
+                            const std::uint64_t jlo = desc_k(st + 2 * TILE_A + TILE_J + kk * 32);
                             mma_f16_ss_pair_elect(d, ahi, jlo, idesc, 1);
                         }
 #endif
@@ -939,7 +955,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 float2 an[SB / 2];                              // previous sub-block's coupling
 #pragma unroll                                                  // to this one (built during its walk)
                 for (int j = 0; j < SB / 2; ++j) an[j] = make_float2(0.0f, 0.0f);
-                for (int t = 0; t < nsub; ++t) {
+                for (int t = 0; t < (up.gemmonly ? 0 : nsub); ++t) {
                     const int k0 = t * SB;
                     const long long tpre = clock64();
                     float old[SB];
@@ -988,7 +1004,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     c_st += clock64() - t0;
                 }
                 dmax = fmaxf(dmax, ctx.dmax);
-                if (JBUFS == 1) mbar_arrive(&ctl.wdone);            // done with this block's triangle
+                if (JBUFS == 1 || up.gemmonly) mbar_arrive(&ctl.wdone);   // done with this block's triangle
                 tc_fence_before();
                 mbar_arrive_cluster(tmem_empty_leader + buf * 8);   // the leader's MMA reuses the buffer
                 if (b == nb - 1) {
@@ -1071,7 +1087,14 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                 c_tw += t1 - t0;
                 const std::uint32_t tacc = tmem + lane_t + buf * TB;
                 bool staged = false;
-                for (int t = HT0; t <= nsub + HT0 - 1; ++t) {
+                if (up.gemmonly && JBUFS == 2) {
+                    // the walkers are past block g-1 (so they have taken that buffer's previous phase)
+                    if (g >= 1) mbar_wait(&ctl.wdone, (g - 1) & 1);
+                    const int nb0 = (b + 1 == nb) ? 0 : b0 + TB;
+                    issue_jtri(Jtri0 + ((g + 1) & 1) * (SMEM_TRI / 4), a.J32, np, nb0, ht);
+                    cp_async_arrive_noinc(&ctl.jready[(g + 1) & 1]);
+                }
+                for (int t = HT0; !up.gemmonly && t <= nsub + HT0 - 1; ++t) {
                     // target sub-block t (t < nsub); D-event for sub-block t-HT0 (always for
                     // sub-block 0, else only while t < nsub) -- mirrors the walker's arrivals
                     const bool target = t < nsub;
@@ -1099,7 +1122,8 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                                     }
                         }
                         // Deltas already final: sub-blocks 0 .. t-HT0-1
-                        for (int u = 0; u + HT0 + 1 <= t; ++u) rect_mma(f, tdel, jtri, u, t, jup, lane);
+                        if (!up.nohelp)
+                            for (int u = 0; u + HT0 + 1 <= t; ++u) rect_mma(f, tdel, jtri, u, t, jup, lane);
                     }
 #else
                     float2 pf[SB / 2];
@@ -1133,7 +1157,7 @@ relax_dense_umma_kernel(RelaxArgs a, UmmaParams up, const __grid_constant__ CUte
                     }
                     if (!target) break;
 #if MARS_HELPER_MMA
-                    rect_mma(f, tdel, jtri, t - HT0, t, jup, lane);
+                    if (!up.nohelp) rect_mma(f, tdel, jtri, t - HT0, t, jup, lane);
 #pragma unroll
                     for (int m = 0; m < 2; ++m) {
 #pragma unroll
@@ -1277,8 +1301,10 @@ cudaError_t launch_relax_dense_umma(const RelaxArgs& a, const UmmaLaunch& u, int
     const char* sp = std::getenv("MARS_UMMA_SPOL");
     const char* jp = std::getenv("MARS_UMMA_JPOL");
     const char* nw = std::getenv("MARS_UMMA_NOWB");
+    const char* nh = std::getenv("MARS_UMMA_NOHELP");
     UmmaParams up{u.xpart, u.s_hi, u.s_hi, u.s_lo, a.np / TB, pf ? std::atoi(pf) : 0, sp ? std::atoi(sp) : 2,
-                  jp ? std::atoi(jp) : 1, nw ? std::atoi(nw) : 0};
+                  jp ? std::atoi(jp) : 1, nw ? std::atoi(nw) : 0, nh ? std::atoi(nh) : 0,
+                  std::getenv("MARS_UMMA_GEMMONLY") ? std::atoi(std::getenv("MARS_UMMA_GEMMONLY")) : 0};
     const int split = clamp_split(u.split);
     if (a.np % TB != 0 || grid % (2 * split) != 0 || (a.np / KC) % split != 0) return cudaErrorInvalidValue;
     UmmaKernel kern = umma_kernel(split, u.jlo);
